@@ -1,0 +1,53 @@
+# Build recipe for the B200 state-vector simulator.
+#   libqsv.so    sm_100a CUDA kernels + the C-ABI (include/qsv.h)
+#   libqsim.so   C++ host library: reference API, DAGC/SMGP planner, facade (include/qsim_c.h)
+#   liboracle.so CPU restatement used only by tests / bench baselines (oracle/)
+#   oracle/_ref  the reference's own gate.cpp + memtrack.cpp (only where /root/reference exists)
+NVCC     ?= nvcc
+CXX      ?= g++
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+PKG      := paper_2509_04955_b200
+LIB      := $(PKG)/lib
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Iinclude -Xcompiler -fPIC,-O3 --expt-relaxed-constexpr
+CXXFLAGS := -std=c++20 -O3 -fPIC -Wall -Wextra -Iinclude -I$(PKG)/cpp/include -I/usr/local/cuda/include
+CU_SRC   := $(wildcard $(PKG)/csrc/*.cu)
+CU_OBJ   := $(patsubst $(PKG)/csrc/%.cu,build/cu/%.o,$(CU_SRC))
+CPP_SRC  := $(wildcard $(PKG)/cpp/src/*.cpp)
+CPP_OBJ  := $(patsubst $(PKG)/cpp/src/%.cpp,build/cpp/%.o,$(CPP_SRC))
+HDRS     := $(wildcard include/*.h) $(wildcard $(PKG)/csrc/*.h) $(wildcard $(PKG)/cpp/include/qsim/*.hpp)
+TESTS_CPP:= $(wildcard tests/cpp/*.cpp)
+TEST_BIN := $(patsubst tests/cpp/%.cpp,build/tests/%,$(TESTS_CPP))
+
+all: $(LIB)/libqsv.so $(LIB)/libqsim.so oracle/liboracle.so ref tests-cpp
+
+build/cu/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB)/libqsv.so: $(CU_OBJ)
+	@mkdir -p $(LIB)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lnccl
+
+build/cpp/%.o: $(PKG)/cpp/src/%.cpp $(HDRS)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(LIB)/libqsim.so: $(CPP_OBJ) $(LIB)/libqsv.so
+	$(CXX) -shared -o $@ $(CPP_OBJ) -L$(LIB) -lqsv -Wl,-rpath,'$$ORIGIN' -lpthread
+
+oracle/liboracle.so: oracle/oracle.cpp oracle/oracle.h
+	$(CXX) -std=c++20 -O3 -march=x86-64-v3 -fPIC -shared -Wall -Wextra $< -o $@ -lpthread
+
+ref:
+	@./oracle/build_ref.sh
+
+build/tests/%: tests/cpp/%.cpp $(LIB)/libqsim.so $(HDRS)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) $< -o $@ -L$(LIB) -lqsim -lqsv -Wl,-rpath,'$$ORIGIN/../../$(LIB)'
+
+tests-cpp: $(TEST_BIN)
+
+clean:
+	rm -rf build $(LIB)/*.so oracle/liboracle.so oracle/_ref
+
+.PHONY: all ref clean tests-cpp

@@ -1,0 +1,112 @@
+/*
+ * qsim_c.h — plain-C facade of the qsim host library (libqsim.so) for callers
+ * that cannot use the C++ API (Python ctypes in tests/ and bench.py, other
+ * FFIs).  It exposes the reference-level objects — circuits, generators, the
+ * DAGC/SMGP planner and the device engine — with the same error convention as
+ * include/qsv.h: 0 on success, negative QSV_E_* codes on failure, message in
+ * qsim_last_error() (thread-local).  C++ exceptions never cross this boundary.
+ *
+ * Reference interfaces mirrored (SPEC = /root/reference/SPEC.md):
+ *   qsim_circuit_*   Circuit / Gate / from_mnemonic (ref gate.hpp:33-92)
+ *   qsim_circuit_generate  gen_qft/gen_qaoa/gen_hea + random / uccsd
+ *   qsim_run_local_host    run_local on host amplitudes
+ *   qsim_engine_*          run_local / run_distributed with a device-resident state
+ */
+#ifndef QSIM_C_H
+#define QSIM_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qsim_circuit qsim_circuit;
+typedef struct qsim_engine qsim_engine;
+
+/* Flat gate record (layout shared with the test oracle's orc_gate). */
+typedef struct qsim_gate_rec {
+    int32_t arity;          /* 0 = barrier                                     */
+    int32_t nctrl;
+    int32_t targets[8];
+    int32_t controls[8];
+    int64_t mat_off;        /* complex offset of the 4^arity matrix in the pool */
+} qsim_gate_rec;
+
+typedef struct qsim_plan_opts {
+    int32_t tile_k;           /* tile qubits per pass (<= 11)                   */
+    int32_t min_low;          /* contiguous low qubits in every tile             */
+    int32_t fuse_k;           /* largest fused dense block (<= 5)               */
+    int32_t fusion;           /* DAGC on (1) / off (0)                          */
+    int32_t multi_op_passes;  /* SMGP multi-block passes on (1) / off (0)       */
+    int32_t chunk_log2;       /* BBOP batch 2^b amplitudes                      */
+    int32_t nbuf;             /* BBOP buffers B                                 */
+    int32_t reserved;
+    double pass_budget;       /* DP cost units per amplitude per pass           */
+} qsim_plan_opts;
+
+typedef struct qsim_plan_stats {
+    int64_t gates_in, ops_lowered, ops_fused, passes, swaps;
+    double cost_units;
+    int32_t max_dense_k, n, n_local, nsteps;
+} qsim_plan_stats;
+
+const char* qsim_last_error(void);
+void qsim_default_opts(qsim_plan_opts* out);
+
+/* ---- circuits ---- */
+int qsim_circuit_generate(const char* spec, qsim_circuit** out);
+int qsim_circuit_new(int n, qsim_circuit** out);
+int qsim_circuit_add(qsim_circuit* c, const char* mnemonic, const double* params, int nparams,
+                     const int* qubits, int nqubits);
+int qsim_circuit_add_unitary(qsim_circuit* c, int k, const int* targets, int nctrl, const int* controls,
+                             const double* mat, const char* label);
+int qsim_circuit_add_barrier(qsim_circuit* c, int nqubits, const int* qubits);
+/* n, number of records (gates incl. barriers), pool length in complex entries */
+int qsim_circuit_info(const qsim_circuit* c, int* n, int64_t* nrecs, int64_t* pool_len);
+int qsim_circuit_export(const qsim_circuit* c, qsim_gate_rec* recs, double* pool);
+/* Gates [begin, end) as a new circuit (used for bounded CPU-baseline samples). */
+int qsim_circuit_slice(const qsim_circuit* c, int64_t begin, int64_t end, qsim_circuit** out);
+/* The fused op list the planner would execute, as a circuit of FUSED gates. */
+int qsim_circuit_fused(const qsim_circuit* c, const qsim_plan_opts* opts, qsim_circuit** out);
+/* Plans for n_local local qubits (-1 = all) and validates the program with the
+ * device library's host-side compiler; fills stats.  No GPU needed. */
+int qsim_circuit_plan(const qsim_circuit* c, const qsim_plan_opts* opts, int n_local, int rank,
+                      qsim_plan_stats* stats);
+void qsim_circuit_free(qsim_circuit* c);
+
+/* ---- engine: one rank's GPU, a planned circuit and its device state ---- */
+int qsim_engine_create(const qsim_circuit* c, const qsim_plan_opts* opts, int device, int rank,
+                       int nranks, const void* comm_id, qsim_engine** out);
+void qsim_engine_free(qsim_engine* e);
+int qsim_engine_stats(qsim_engine* e, qsim_plan_stats* out);
+void* qsim_engine_stream(qsim_engine* e);      /* cudaStream_t */
+void* qsim_engine_qsv_state(qsim_engine* e);   /* qsv_state*   */
+void* qsim_engine_qsv_program(qsim_engine* e); /* qsv_program* */
+int qsim_engine_set_basis(qsim_engine* e, uint64_t global_index);
+int qsim_engine_upload(qsim_engine* e, const double* amps, uint64_t offset, uint64_t count);
+int qsim_engine_download(qsim_engine* e, double* amps, uint64_t offset, uint64_t count);
+int qsim_engine_run(qsim_engine* e);           /* enqueue (asynchronous) */
+int qsim_engine_sync(qsim_engine* e);
+int qsim_engine_time(qsim_engine* e, int iters, float* ms);
+int qsim_engine_norm_sq(qsim_engine* e, double* out);
+int qsim_engine_max_abs_diff(qsim_engine* e, const double* ref, uint64_t offset, uint64_t count,
+                             double* out);
+int qsim_engine_check_qft(qsim_engine* e, uint64_t x, double* out);
+int qsim_engine_digest(qsim_engine* e, uint64_t* out);
+int qsim_engine_nsteps(qsim_engine* e);
+int qsim_engine_step_info(qsim_engine* e, int i, int* kind, int* nops, double* hbm_bytes, double* flops,
+                          double* nvl_bytes);
+int qsim_engine_profile(qsim_engine* e, float* ms_per_step);
+
+/* ---- reference-facing single call: run_local on host amplitudes ---------
+ * Uploads `amps` (2^n interleaved complex, ideally pinned), runs the planned
+ * circuit on device 0, downloads the result into `amps`. */
+int qsim_run_local_host(const qsim_circuit* c, const qsim_plan_opts* opts, double* amps);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

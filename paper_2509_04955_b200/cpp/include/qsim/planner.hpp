@@ -1,0 +1,87 @@
+// The B200 circuit planner: the host pass that turns a Circuit into the
+// device program uploaded through include/qsv.h.
+//
+//   lower()     gate -> op: DENSE (general), DIAG (diagonal, incl. CP/CZ/RZ/S/T;
+//               controlled diagonals with a single non-unit entry become a
+//               "phase on all-ones pattern"), XPERM (X / CX).
+//   fuse_ops()  DAGC re-targeted to the fp64/HBM roofline (PAPER:391-483,
+//               SPEC:232-331): greedy merge of each op into the latest op on
+//               its qubits when the merged block stays <= fuse_k qubits and the
+//               per-amplitude DP cost does not grow (same-support runs,
+//               CU consolidation, Kronecker products are all special cases).
+//               Barriers are fences.
+//   pack()      SMGP re-designed as multi-block passes: ops are
+//               packed, in program order, into passes whose dense targets fit
+//               one 2^K-amplitude tile (>= 2^5 contiguous low amplitudes) and
+//               whose DP cost per amplitude stays under the roofline budget, so
+//               each pass is one HBM round trip.
+//   partition   (multi-GPU) the top log2(P) physical qubits are global
+//               (PAPER:280); a dense target on a global qubit
+//               inserts a BBOP qubit swap with a local victim (swap.cu).
+#pragma once
+
+#include "qsim/circuit.hpp"
+#include "qsv.h"
+
+#include <string>
+#include <vector>
+
+namespace qsim {
+
+enum class OpKind { Dense, Diag, XPerm, Fence };
+
+// One lowered op on LOGICAL qubits.
+struct Op {
+    OpKind kind = OpKind::Dense;
+    std::vector<int> qubits;    // Dense/XPerm: targets; Diag: diagonal qubits (qubits[p] = bit p)
+    std::vector<int> controls;  // all must be 1
+    std::vector<Amp> data;      // Dense: 4^k entries row-major; Diag: 2^k entries
+    int first_gate = -1;        // provenance (gate index range)
+    int last_gate = -1;
+    int ngates = 0;             // source gates merged into this op
+};
+
+struct PlanOptions {
+    int tile_k = 10;          // tile qubits per pass (<= 11)
+    int min_low = 5;          // contiguous low run: 2^5 amplitudes = 512-B DRAM runs
+    int fuse_k = 3;           // largest dense block fusion may create (<= QSV_MAX_DENSE_K)
+    bool fusion = true;       // DAGC on/off (BASELINE configs[1]: "contraction on vs off")
+    bool multi_op_passes = true;  // SMGP on/off: off = one op per pass
+    double pass_budget = 64;  // DP cost units per amplitude allowed in one pass
+    int n_local = -1;         // local qubits per rank (-1: all, single GPU)
+    int chunk_log2 = 22;      // BBOP batch: 2^b amplitudes per swap message
+    int nbuf = 2;             // BBOP buffers B (default 2)
+};
+
+struct PlanStats {
+    std::size_t gates_in = 0;      // gates excluding barriers (gates/s numerator)
+    std::size_t ops_lowered = 0;
+    std::size_t ops_fused = 0;     // ops after fusion
+    std::size_t passes = 0;
+    std::size_t swaps = 0;
+    double cost_units = 0;         // sum of op costs (DP units / amplitude)
+    int max_dense_k = 0;
+};
+
+struct Plan {
+    int n = 0;
+    int n_local = 0;
+    std::vector<qsv_step_desc> steps;
+    std::vector<qsv_op_desc> ops;
+    std::vector<double> pool;          // complex entries, re/im interleaved
+    std::vector<Op> fused;             // fused ops (logical qubits), for inspection/tests
+    PlanStats stats;
+};
+
+// Classification helpers.
+std::vector<Op> lower(const Circuit& c);
+std::vector<Op> fuse_ops(const std::vector<Op>& ops, const PlanOptions& opt);
+// Relative DP cost per amplitude of one op (the packing / fusion currency).
+double op_cost(const Op& op);
+// Builds the full plan (lower -> fuse -> partition/swaps -> pack).
+Plan make_plan(const Circuit& c, const PlanOptions& opt);
+// Re-expresses fused ops as a Circuit of FUSED gates (for oracle checks of the
+// fusion, SPEC:312 semantic preservation).
+Circuit ops_to_circuit(int n, const std::vector<Op>& ops);
+
+} // namespace qsim

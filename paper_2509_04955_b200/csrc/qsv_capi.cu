@@ -1,0 +1,949 @@
+// C-ABI implementation of include/qsv.h: contexts, state shards, program
+// upload/compilation, reductions and checks.  The pass kernel lives in
+// pass_kernel.cu and the qubit swap in swap.cu.
+//
+// Nothing in this file has a CPU compute fallback: every amplitude operation
+// is a CUDA kernel; a missing device fails with QSV_E_NODEV.
+#include "qsv_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+namespace qsv {
+
+namespace {
+thread_local std::string t_err;
+}
+
+void set_error(const std::string& msg) { t_err = msg; }
+
+} // namespace qsv
+
+using qsv::set_error;
+
+#define QSV_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            set_error(std::string(#call) + ": " + cudaGetErrorString(e_));              \
+            return e_ == cudaErrorMemoryAllocation ? QSV_E_NOMEM : QSV_E_CUDA;          \
+        }                                                                               \
+    } while (0)
+
+#define QSV_REQUIRE(cond, msg)          \
+    do {                                \
+        if (!(cond)) {                  \
+            set_error(msg);             \
+            return QSV_E_ARG;           \
+        }                               \
+    } while (0)
+
+// ======================================================================= kernels
+namespace {
+
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ void kahan_add(double& s, double& c, double x) {
+    const double y = x - c;
+    const double t = s + y;
+    c = (t - s) - y;
+    s = t;
+}
+
+// Per-thread Kahan sums of |a|^2, then a block tree: the 2^n-term norm stays
+// well inside the 1e-12 budget (SURVEY §7 hard part 6).
+__global__ void norm_partial_kernel(const double2* __restrict__ a, uint64_t n, double* partials) {
+    double s = 0.0, c = 0.0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double2 v = __ldcs(a + i);
+        kahan_add(s, c, fma(v.x, v.x, v.y * v.y));
+    }
+    __shared__ double sh[32];
+    double v = s - c;
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x % 32 == 0)
+        sh[threadIdx.x / 32] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0, tc = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w)
+            kahan_add(t, tc, sh[w]);
+        partials[blockIdx.x] = t;
+    }
+}
+
+__global__ void sum_partials_kernel(const double* partials, int n, double* out) {
+    double s = 0.0, c = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        kahan_add(s, c, partials[i]);
+    __shared__ double sh[kRedThreads];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0, tc = 0.0;
+        for (int i = 0; i < static_cast<int>(blockDim.x); ++i)
+            kahan_add(t, tc, sh[i]);
+        *out = t;
+    }
+}
+
+__global__ void max_partials_kernel(const double* partials, int n, double* out) {
+    double m = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        m = fmax(m, partials[i]);
+    __shared__ double sh[kRedThreads];
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < static_cast<int>(blockDim.x); ++i)
+            t = fmax(t, sh[i]);
+        *out = t;
+    }
+}
+
+__device__ void block_max_store(double m, double* partials) {
+    __shared__ double sh[32];
+    for (int o = 16; o > 0; o >>= 1)
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x % 32 == 0)
+        sh[threadIdx.x / 32] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w)
+            t = fmax(t, sh[w]);
+        partials[blockIdx.x] = t;
+    }
+}
+
+__global__ void diff_partial_kernel(const double2* __restrict__ a, const double2* __restrict__ b,
+                                    uint64_t n, double* partials) {
+    double m = 0.0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double2 x = a[i], y = b[i];
+        const double d = hypot(x.x - y.x, x.y - y.y);
+        m = (d != d) ? INFINITY : fmax(m, d);  // NaN poisons the check
+    }
+    block_max_store(m, partials);
+}
+
+// Analytic QFT of |x>: psi[y] = exp(2 pi i x y / 2^n) / 2^{n/2}.  The phase is
+// reduced exactly in integers (x*y mod 2^n via uint64 wrap-around).
+__global__ void qft_check_kernel(const double2* __restrict__ a, uint64_t n_amps, uint64_t rank_base,
+                                 int n_total, uint64_t x, double* partials) {
+    const uint64_t mask = (n_total >= 64) ? ~0ull : ((1ull << n_total) - 1ull);
+    const double scale = exp2(-0.5 * n_total);
+    const double inv = exp2(1.0 - n_total);  // sincospi(2 * p / 2^n) = sincospi(p * 2^{1-n})
+    double m = 0.0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_amps;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t y = rank_base | i;
+        const uint64_t p = (x * y) & mask;
+        double s, c;
+        sincospi(static_cast<double>(p) * inv, &s, &c);
+        const double2 v = a[i];
+        const double d = hypot(v.x - c * scale, v.y - s * scale);
+        m = (d != d) ? INFINITY : fmax(m, d);
+    }
+    block_max_store(m, partials);
+}
+
+__global__ void digest_kernel(const unsigned long long* __restrict__ w, uint64_t nwords,
+                              unsigned long long* out) {
+    unsigned long long x = 0, s = 0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nwords;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const unsigned long long v = w[i];
+        x ^= v * 0x9E3779B97F4A7C15ull + i;
+        s += v;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        x ^= __shfl_xor_sync(0xffffffffu, x, o);
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+    }
+    if (threadIdx.x % 32 == 0) {
+        atomicXor(out, x);
+        atomicAdd(out + 1, s);
+    }
+}
+
+__global__ void set_one_kernel(double2* p) { *p = make_double2(1.0, 0.0); }
+
+int reduce_grid(const qsv_ctx* ctx) { return ctx->sm_count * 8; }
+
+int ensure_partials(qsv_ctx* ctx) {
+    const size_t need = static_cast<size_t>(reduce_grid(ctx)) + 8;
+    if (ctx->partials_cap >= need)
+        return QSV_OK;
+    if (ctx->d_partials)
+        cudaFree(ctx->d_partials);
+    QSV_CUDA(cudaMalloc(&ctx->d_partials, need * sizeof(double)));
+    ctx->partials_cap = need;
+    return QSV_OK;
+}
+
+// Finish a max-style reduction of `grid` partials into *out (synchronous).
+int finish_max(qsv_ctx* ctx, int grid, double* out) {
+    max_partials_kernel<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_partials, grid,
+                                                           ctx->d_partials + ctx->partials_cap - 1);
+    QSV_CUDA(cudaGetLastError());
+    QSV_CUDA(cudaMemcpyAsync(ctx->h_result, ctx->d_partials + ctx->partials_cap - 1, sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    QSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = ctx->h_result[0];
+    return QSV_OK;
+}
+
+bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
+
+int log2i(int x) {
+    int l = 0;
+    while ((1 << l) < x)
+        ++l;
+    return l;
+}
+
+} // namespace
+
+// ======================================================================= devices
+extern "C" int qsv_device_count(int* n) {
+    QSV_REQUIRE(n != nullptr, "qsv_device_count: null output");
+    int c = 0;
+    cudaError_t e = cudaGetDeviceCount(&c);
+    if (e != cudaSuccess) {
+        *n = 0;
+        set_error(std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+        return QSV_E_NODEV;
+    }
+    *n = c;
+    return QSV_OK;
+}
+
+extern "C" int qsv_comm_unique_id(void* out) {
+    QSV_REQUIRE(out != nullptr, "qsv_comm_unique_id: null output");
+    static_assert(sizeof(ncclUniqueId) == QSV_NCCL_ID_BYTES, "NCCL id size");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+        return QSV_E_NCCL;
+    }
+    std::memcpy(out, &id, sizeof(id));
+    return QSV_OK;
+}
+
+extern "C" int qsv_ctx_create(int device, int rank, int nranks, const void* comm_id, qsv_ctx** out) {
+    QSV_REQUIRE(out != nullptr, "qsv_ctx_create: null output");
+    QSV_REQUIRE(is_pow2(nranks), "qsv_ctx_create: nranks must be a power of two (SPEC:341)");
+    QSV_REQUIRE(rank >= 0 && rank < nranks, "qsv_ctx_create: rank out of range");
+    QSV_REQUIRE(nranks == 1 || comm_id != nullptr, "qsv_ctx_create: nranks > 1 needs a comm id");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set_error("qsv_ctx_create: no CUDA device (the simulator has no CPU fallback)");
+        return QSV_E_NODEV;
+    }
+    QSV_REQUIRE(device >= 0 && device < ndev, "qsv_ctx_create: device index out of range");
+    QSV_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    QSV_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+        set_error("qsv_ctx_create: device is not sm_100-class (built for sm_100a only)");
+        return QSV_E_NODEV;
+    }
+    auto* ctx = new qsv_ctx();
+    ctx->device = device;
+    ctx->rank = rank;
+    ctx->nranks = nranks;
+    ctx->sm_count = prop.multiProcessorCount;
+    QSV_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    QSV_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    QSV_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    QSV_CUDA(cudaEventCreateWithFlags(&ctx->ev_a, cudaEventDisableTiming));
+    QSV_CUDA(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
+    QSV_CUDA(cudaMallocHost(&ctx->h_result, 4 * sizeof(double)));
+    if (nranks > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, comm_id, sizeof(id));
+        ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
+        if (r != ncclSuccess) {
+            set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+            delete ctx;
+            return QSV_E_NCCL;
+        }
+    }
+    *out = ctx;
+    return QSV_OK;
+}
+
+extern "C" int qsv_ctx_destroy(qsv_ctx* ctx) {
+    if (!ctx)
+        return QSV_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm)
+        ncclCommDestroy(ctx->comm);
+    if (ctx->d_partials) cudaFree(ctx->d_partials);
+    if (ctx->d_stage) cudaFree(ctx->d_stage);
+    if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+    if (ctx->h_result) cudaFreeHost(ctx->h_result);
+    cudaEventDestroy(ctx->ev_a);
+    cudaEventDestroy(ctx->ev_b);
+    cudaStreamDestroy(ctx->stream);
+    cudaStreamDestroy(ctx->comm_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    delete ctx;
+    return QSV_OK;
+}
+
+extern "C" void* qsv_ctx_stream(qsv_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+extern "C" int qsv_sync(qsv_ctx* ctx) {
+    QSV_REQUIRE(ctx != nullptr, "qsv_sync: null context");
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    QSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    return QSV_OK;
+}
+
+extern "C" const char* qsv_last_error(void) { return qsv::t_err.c_str(); }
+
+// ======================================================================= states
+extern "C" int qsv_state_alloc(qsv_ctx* ctx, int n_local, qsv_state** out, size_t* bytes) {
+    QSV_REQUIRE(ctx != nullptr && out != nullptr, "qsv_state_alloc: null argument");
+    QSV_REQUIRE(n_local >= 1 && n_local <= 40, "qsv_state_alloc: n_local must be in [1, 40]");
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    auto* st = new qsv_state();
+    st->ctx = ctx;
+    st->n_local = n_local;
+    st->size = 1ull << n_local;
+    const size_t b = sizeof(double2) * st->size;
+    cudaError_t e = cudaMalloc(&st->amps, b);
+    if (e != cudaSuccess) {
+        delete st;
+        set_error("qsv_state_alloc: cudaMalloc of " + std::to_string(b) + " bytes failed: " +
+                  cudaGetErrorString(e));
+        return QSV_E_NOMEM;
+    }
+    if (bytes)
+        *bytes = b;
+    *out = st;
+    return QSV_OK;
+}
+
+extern "C" int qsv_state_free(qsv_state* st) {
+    if (!st)
+        return QSV_OK;
+    cudaSetDevice(st->ctx->device);
+    cudaStreamSynchronize(st->ctx->stream);
+    cudaFree(st->amps);
+    delete st;
+    return QSV_OK;
+}
+
+extern "C" int qsv_state_set_basis(qsv_state* st, uint64_t global_index) {
+    QSV_REQUIRE(st != nullptr, "qsv_state_set_basis: null state");
+    qsv_ctx* ctx = st->ctx;
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    QSV_CUDA(cudaMemsetAsync(st->amps, 0, sizeof(double2) * st->size, ctx->stream));
+    const uint64_t owner = global_index >> st->n_local;
+    QSV_REQUIRE(owner < static_cast<uint64_t>(ctx->nranks), "qsv_state_set_basis: index >= 2^n");
+    if (owner == static_cast<uint64_t>(ctx->rank)) {
+        set_one_kernel<<<1, 1, 0, ctx->stream>>>(st->amps + (global_index & (st->size - 1)));
+        QSV_CUDA(cudaGetLastError());
+    }
+    return QSV_OK;
+}
+
+extern "C" int qsv_state_upload(qsv_state* st, const double* host, uint64_t offset, uint64_t count) {
+    QSV_REQUIRE(st != nullptr && (host != nullptr || count == 0), "qsv_state_upload: null argument");
+    QSV_REQUIRE(offset <= st->size && count <= st->size - offset, "qsv_state_upload: range outside shard");
+    QSV_CUDA(cudaSetDevice(st->ctx->device));
+    QSV_CUDA(cudaMemcpyAsync(st->amps + offset, host, count * sizeof(double2), cudaMemcpyHostToDevice,
+                             st->ctx->stream));
+    return QSV_OK;
+}
+
+extern "C" int qsv_state_download(qsv_state* st, double* host, uint64_t offset, uint64_t count) {
+    QSV_REQUIRE(st != nullptr && (host != nullptr || count == 0), "qsv_state_download: null argument");
+    QSV_REQUIRE(offset <= st->size && count <= st->size - offset, "qsv_state_download: range outside shard");
+    QSV_CUDA(cudaSetDevice(st->ctx->device));
+    QSV_CUDA(cudaMemcpyAsync(host, st->amps + offset, count * sizeof(double2), cudaMemcpyDeviceToHost,
+                             st->ctx->stream));
+    QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    return QSV_OK;
+}
+
+extern "C" int qsv_state_device_ptr(qsv_state* st, void** ptr) {
+    QSV_REQUIRE(st != nullptr && ptr != nullptr, "qsv_state_device_ptr: null argument");
+    *ptr = st->amps;
+    return QSV_OK;
+}
+
+extern "C" int qsv_host_alloc(size_t bytes, void** ptr) {
+    QSV_REQUIRE(ptr != nullptr, "qsv_host_alloc: null output");
+    QSV_CUDA(cudaMallocHost(ptr, bytes));
+    return QSV_OK;
+}
+
+extern "C" int qsv_host_free(void* ptr) {
+    if (ptr)
+        QSV_CUDA(cudaFreeHost(ptr));
+    return QSV_OK;
+}
+
+// ======================================================================= programs
+namespace {
+
+struct BlobBuilder {
+    std::vector<unsigned char> bytes;
+    uint32_t append(const void* p, size_t n) {
+        const size_t at = (bytes.size() + 15) & ~size_t{15};
+        bytes.resize(at + n);
+        std::memcpy(bytes.data() + at, p, n);
+        return static_cast<uint32_t>(at);
+    }
+};
+
+int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
+                 const qsv_op_desc* ops, int nops, const double* pool, size_t pool_len,
+                 qsv::Step& step, std::vector<unsigned char>& blob_out) {
+    using qsv::TileOp;
+    const int K = d.tile_k;
+    QSV_REQUIRE(K >= 1 && K <= 11 && K <= n_local, "pass: tile_k must be in [1, min(11, n_local)]");
+    QSV_REQUIRE(d.nhigh >= 0 && d.nhigh <= QSV_MAX_HIGH && d.nhigh <= K, "pass: bad nhigh");
+    const int L = K - d.nhigh;
+    int tpos_of[64];
+    for (int q = 0; q < 64; ++q)
+        tpos_of[q] = (q < L) ? q : -1;
+    for (int i = 0; i < d.nhigh; ++i) {
+        const int h = d.high[i];
+        QSV_REQUIRE(h >= L && h < n_local, "pass: high tile qubit must be local and above the low run");
+        QSV_REQUIRE(i == 0 || h > d.high[i - 1], "pass: high tile qubits must be ascending");
+        tpos_of[h] = L + i;
+    }
+    QSV_REQUIRE(d.op_begin >= 0 && d.op_count >= 0 && d.op_begin + d.op_count <= nops,
+                "pass: op range outside the op array");
+    step.geom.K = K;
+    step.geom.L = L;
+    step.geom.nhigh = d.nhigh;
+    for (int i = 0; i < d.nhigh; ++i)
+        step.geom.high[i] = d.high[i];
+    step.geom.kmax = 0;
+    step.nops = d.op_count;
+
+    const uint64_t full_mask = (n_total >= 64) ? ~0ull : ((1ull << n_total) - 1ull);
+    const uint64_t rank_bits = static_cast<uint64_t>(rank) << n_local;
+    std::vector<TileOp> tops(d.op_count);
+    struct Payload { int op; std::vector<uint32_t> off; std::vector<double> data; };
+    std::vector<Payload> payloads;
+    double flops = 0.0;
+    const double amps = std::ldexp(1.0, n_local);
+
+    for (int oi = 0; oi < d.op_count; ++oi) {
+        const qsv_op_desc& od = ops[d.op_begin + oi];
+        TileOp t{};
+        t.kind = od.kind;
+        t.k = od.k;
+        QSV_REQUIRE((od.ctrl_mask & ~full_mask) == 0, "op: control bit >= n_total");
+        uint64_t qmask = 0;
+        for (int i = 0; i < od.k; ++i) {
+            const int q = od.qubits[i];
+            QSV_REQUIRE(q >= 0 && q < n_total, "op: qubit out of range");
+            QSV_REQUIRE(!(qmask >> q & 1), "op: duplicate qubit");
+            qmask |= 1ull << q;
+        }
+        QSV_REQUIRE((qmask & od.ctrl_mask) == 0, "op: control overlaps a target (SPEC:51)");
+        // controls: tile-local ones restrict enumeration, the rest are CTA-uniform tests
+        std::vector<int> fix;
+        for (int c = 0; c < n_total; ++c) {
+            if (!(od.ctrl_mask >> c & 1))
+                continue;
+            if (c < n_local && tpos_of[c] >= 0) {
+                t.tctrl |= 1u << tpos_of[c];
+                fix.push_back(tpos_of[c]);
+            } else {
+                t.xctrl |= 1ull << c;
+            }
+        }
+        const int nctrl = __builtin_popcountll(od.ctrl_mask);
+        // fraction of this rank's amplitudes the op touches
+        const bool rank_ok = ((rank_bits & t.xctrl) >> n_local) == ((t.xctrl & ~((1ull << n_local) - 1)) >> n_local);
+        const int local_ctrls = __builtin_popcountll(od.ctrl_mask & ((1ull << n_local) - 1));
+        const double frac = rank_ok ? std::ldexp(1.0, -local_ctrls) : 0.0;
+        (void)nctrl;
+        Payload pl;
+        pl.op = oi;
+        if (od.kind == QSV_OP_DENSE || od.kind == QSV_OP_XPERM) {
+            QSV_REQUIRE(od.k >= 1 && od.k <= (od.kind == QSV_OP_XPERM ? 1 : QSV_MAX_DENSE_K),
+                        "op: dense arity must be in [1, 5] (XPERM: 1)");
+            for (int i = 0; i < od.k; ++i) {
+                const int q = od.qubits[i];
+                QSV_REQUIRE(q < n_local && tpos_of[q] >= 0,
+                            "op: dense/XPERM target " + std::to_string(q) + " is not in the pass tile");
+                t.tpos[i] = static_cast<int8_t>(tpos_of[q]);
+                fix.push_back(tpos_of[q]);
+            }
+            if (od.kind == QSV_OP_DENSE) {
+                const int D = 1 << od.k;
+                QSV_REQUIRE(od.mat_off >= 0 && static_cast<size_t>(od.mat_off) + D * D <= pool_len,
+                            "op: matrix outside the pool");
+                pl.off.resize(D);
+                for (int j = 0; j < D; ++j) {
+                    uint32_t o = 0;
+                    for (int i = 0; i < od.k; ++i)
+                        if (j >> i & 1)
+                            o |= 1u << t.tpos[i];
+                    pl.off[j] = o;
+                }
+                pl.data.assign(pool + 2 * od.mat_off, pool + 2 * (od.mat_off + D * D));
+                step.geom.kmax = std::max(step.geom.kmax, od.k);
+                flops += 8.0 * D * amps * frac;
+            }
+        } else if (od.kind == QSV_OP_DIAG) {
+            QSV_REQUIRE(od.k >= 0 && od.k <= QSV_MAX_DIAG_K, "op: diagonal arity must be in [0, 8]");
+            const int D = 1 << od.k;
+            QSV_REQUIRE(od.mat_off >= 0 && static_cast<size_t>(od.mat_off) + D <= pool_len,
+                        "op: diagonal outside the pool");
+            // in-tile qubits first (ascending tile position), then out-of-tile ones
+            std::vector<int> order;  // new bit -> original bit
+            std::vector<std::pair<int, int>> in;
+            std::vector<int> outb;
+            for (int i = 0; i < od.k; ++i) {
+                const int q = od.qubits[i];
+                if (q < n_local && tpos_of[q] >= 0)
+                    in.push_back({tpos_of[q], i});
+                else
+                    outb.push_back(i);
+            }
+            std::sort(in.begin(), in.end());
+            t.nin = static_cast<int32_t>(in.size());
+            for (auto& pr : in) {
+                t.tmask |= 1u << pr.first;
+                order.push_back(pr.second);
+            }
+            for (size_t j = 0; j < outb.size(); ++j) {
+                t.xbit[j] = static_cast<int8_t>(od.qubits[outb[j]]);
+                order.push_back(outb[j]);
+            }
+            pl.data.resize(2 * D);
+            for (int e = 0; e < D; ++e) {
+                int src = 0;
+                for (int nb = 0; nb < od.k; ++nb)
+                    if (e >> nb & 1)
+                        src |= 1 << order[nb];
+                pl.data[2 * e] = pool[2 * (od.mat_off + src)];
+                pl.data[2 * e + 1] = pool[2 * (od.mat_off + src) + 1];
+            }
+            flops += 6.0 * amps * frac;
+        } else {
+            QSV_REQUIRE(false, "op: unknown kind " + std::to_string(od.kind));
+        }
+        std::sort(fix.begin(), fix.end());
+        QSV_REQUIRE(fix.size() <= sizeof(t.fixpos), "op: too many fixed tile bits");
+        t.nfix = static_cast<int32_t>(fix.size());
+        for (size_t i = 0; i < fix.size(); ++i)
+            t.fixpos[i] = static_cast<int8_t>(fix[i]);
+        tops[oi] = t;
+        if (!pl.data.empty() || !pl.off.empty())
+            payloads.push_back(std::move(pl));
+    }
+    BlobBuilder bb;
+    bb.append(tops.data(), tops.size() * sizeof(TileOp));
+    for (auto& pl : payloads) {
+        TileOp& t = tops[pl.op];
+        if (!pl.off.empty())
+            t.off_byte = bb.append(pl.off.data(), pl.off.size() * sizeof(uint32_t));
+        if (!pl.data.empty())
+            t.mat_byte = bb.append(pl.data.data(), pl.data.size() * sizeof(double));
+    }
+    std::memcpy(bb.bytes.data(), tops.data(), tops.size() * sizeof(TileOp));
+    bb.bytes.resize((bb.bytes.size() + 15) & ~size_t{15});
+    QSV_REQUIRE(bb.bytes.size() <= qsv::kMaxBlobBytes,
+                "pass: ops + matrices exceed the per-pass shared-memory budget (" +
+                    std::to_string(bb.bytes.size()) + " > " + std::to_string(qsv::kMaxBlobBytes) + " B)");
+    step.blob_bytes = static_cast<uint32_t>(bb.bytes.size());
+    step.hbm_bytes = 32.0 * amps;
+    step.flops = flops;
+    blob_out = std::move(bb.bytes);
+    return QSV_OK;
+}
+
+} // namespace
+
+extern "C" int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local, const qsv_step_desc* steps,
+                                  int nsteps, const qsv_op_desc* ops, int nops, const double* pool,
+                                  size_t pool_len, qsv_program** out) {
+    QSV_REQUIRE(ctx != nullptr && out != nullptr, "qsv_program_create: null argument");
+    QSV_REQUIRE(nsteps >= 0 && (steps != nullptr || nsteps == 0), "qsv_program_create: bad steps");
+    QSV_REQUIRE(nops >= 0 && (ops != nullptr || nops == 0), "qsv_program_create: bad ops");
+    QSV_REQUIRE(pool != nullptr || pool_len == 0, "qsv_program_create: null pool");
+    QSV_REQUIRE(n_total >= 1 && n_total <= QSV_MAX_QUBITS, "qsv_program_create: bad n_total");
+    QSV_REQUIRE(n_total - n_local == log2i(ctx->nranks) && (1 << (n_total - n_local)) == ctx->nranks,
+                "qsv_program_create: n_total - n_local must equal log2(nranks)");
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    auto* prog = new qsv_program();
+    prog->ctx = ctx;
+    prog->n_total = n_total;
+    prog->n_local = n_local;
+    std::vector<unsigned char> all;
+    for (int i = 0; i < nsteps; ++i) {
+        qsv::Step s;
+        s.desc = steps[i];
+        if (steps[i].kind == QSV_STEP_PASS) {
+            std::vector<unsigned char> blob;
+            int rc = compile_pass(steps[i], n_total, n_local, ctx->rank, ops, nops, pool, pool_len, s, blob);
+            if (rc != QSV_OK) {
+                set_error("step " + std::to_string(i) + ": " + qsv_last_error());
+                delete prog;
+                return rc;
+            }
+            s.blob_off = all.size();
+            all.insert(all.end(), blob.begin(), blob.end());
+        } else if (steps[i].kind == QSV_STEP_SWAP) {
+            const qsv_step_desc& d = steps[i];
+            if (!(d.swap_global >= n_local && d.swap_global < n_total && d.swap_local >= 0 &&
+                  d.swap_local < n_local && d.chunk_log2 >= 0 && d.chunk_log2 <= n_local - 1 &&
+                  d.nbuf >= 1 && d.nbuf <= 8)) {
+                delete prog;
+                set_error("step " + std::to_string(i) + ": bad swap (global/local/chunk/nbuf)");
+                return QSV_E_ARG;
+            }
+            s.nvl_bytes = 16.0 * std::ldexp(1.0, n_local - 1);
+            s.hbm_bytes = 4.0 * s.nvl_bytes;  // read+write of the sent and the received half
+            prog->has_collective = true;
+        } else {
+            delete prog;
+            set_error("step " + std::to_string(i) + ": unknown step kind");
+            return QSV_E_ARG;
+        }
+        prog->steps.push_back(s);
+    }
+    if (!all.empty()) {
+        cudaError_t e = cudaMalloc(&prog->d_blobs, all.size());
+        if (e != cudaSuccess) {
+            delete prog;
+            set_error(std::string("qsv_program_create: cudaMalloc: ") + cudaGetErrorString(e));
+            return QSV_E_NOMEM;
+        }
+        e = cudaMemcpy(prog->d_blobs, all.data(), all.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(prog->d_blobs);
+            delete prog;
+            set_error(std::string("qsv_program_create: upload: ") + cudaGetErrorString(e));
+            return QSV_E_CUDA;
+        }
+        prog->blob_total = all.size();
+    }
+    *out = prog;
+    return QSV_OK;
+}
+
+extern "C" int qsv_program_validate(int n_total, int n_local, int rank, const qsv_step_desc* steps,
+                                    int nsteps, const qsv_op_desc* ops, int nops, const double* pool,
+                                    size_t pool_len) {
+    QSV_REQUIRE(nsteps >= 0 && (steps != nullptr || nsteps == 0), "qsv_program_validate: bad steps");
+    QSV_REQUIRE(nops >= 0 && (ops != nullptr || nops == 0), "qsv_program_validate: bad ops");
+    QSV_REQUIRE(n_total >= 1 && n_total <= QSV_MAX_QUBITS && n_local >= 1 && n_local <= n_total,
+                "qsv_program_validate: bad sizes");
+    QSV_REQUIRE(rank >= 0 && (static_cast<uint64_t>(rank) >> (n_total - n_local)) == 0,
+                "qsv_program_validate: rank out of range");
+    for (int i = 0; i < nsteps; ++i) {
+        if (steps[i].kind == QSV_STEP_PASS) {
+            qsv::Step s;
+            std::vector<unsigned char> blob;
+            const int rc = compile_pass(steps[i], n_total, n_local, rank, ops, nops, pool, pool_len, s, blob);
+            if (rc != QSV_OK) {
+                set_error("step " + std::to_string(i) + ": " + qsv_last_error());
+                return rc;
+            }
+        } else if (steps[i].kind == QSV_STEP_SWAP) {
+            const qsv_step_desc& d = steps[i];
+            QSV_REQUIRE(d.swap_global >= n_local && d.swap_global < n_total && d.swap_local >= 0 &&
+                            d.swap_local < n_local && d.chunk_log2 >= 0 && d.chunk_log2 <= n_local - 1 &&
+                            d.nbuf >= 1 && d.nbuf <= 8,
+                        "step " + std::to_string(i) + ": bad swap (global/local/chunk/nbuf)");
+        } else {
+            QSV_REQUIRE(false, "step " + std::to_string(i) + ": unknown step kind");
+        }
+    }
+    return QSV_OK;
+}
+
+extern "C" int qsv_program_time(qsv_state* st, qsv_program* prog, int iters, float* ms) {
+    QSV_REQUIRE(st != nullptr && prog != nullptr && ms != nullptr && iters >= 1, "qsv_program_time: bad argument");
+    qsv_ctx* ctx = st->ctx;
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    cudaEvent_t a, b;
+    QSV_CUDA(cudaEventCreate(&a));
+    QSV_CUDA(cudaEventCreate(&b));
+    QSV_CUDA(cudaEventRecord(a, ctx->stream));
+    int rc = QSV_OK;
+    for (int i = 0; i < iters && rc == QSV_OK; ++i)
+        rc = qsv_program_run(st, prog);
+    QSV_CUDA(cudaEventRecord(b, ctx->stream));
+    QSV_CUDA(cudaEventSynchronize(b));
+    QSV_CUDA(cudaEventElapsedTime(ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return rc;
+}
+
+extern "C" int qsv_program_free(qsv_program* prog) {
+    if (!prog)
+        return QSV_OK;
+    cudaSetDevice(prog->ctx->device);
+    cudaStreamSynchronize(prog->ctx->stream);
+    for (auto& kv : prog->graphs)
+        cudaGraphExecDestroy(kv.second);
+    if (prog->d_blobs)
+        cudaFree(prog->d_blobs);
+    delete prog;
+    return QSV_OK;
+}
+
+namespace {
+
+int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
+    qsv_ctx* ctx = st->ctx;
+    const uint64_t rank_base = static_cast<uint64_t>(ctx->rank) << st->n_local;
+    for (size_t i = 0; i < prog->steps.size(); ++i) {
+        const qsv::Step& s = prog->steps[i];
+        if (evs)
+            QSV_CUDA(cudaEventRecord(evs[i], ctx->stream));
+        if (s.desc.kind == QSV_STEP_PASS) {
+            QSV_CUDA(qsv::launch_pass(st, s, prog->d_blobs + s.blob_off, rank_base, ctx->stream));
+        } else {
+            const int rc = qsv::run_swap(st, s.desc.swap_global, s.desc.swap_local, s.desc.chunk_log2,
+                                         s.desc.nbuf);
+            if (rc != QSV_OK)
+                return rc;
+        }
+    }
+    if (evs)
+        QSV_CUDA(cudaEventRecord(evs[prog->steps.size()], ctx->stream));
+    return QSV_OK;
+}
+
+} // namespace
+
+extern "C" int qsv_program_run(qsv_state* st, qsv_program* prog) {
+    QSV_REQUIRE(st != nullptr && prog != nullptr, "qsv_program_run: null argument");
+    QSV_REQUIRE(st->ctx == prog->ctx, "qsv_program_run: state and program belong to different contexts");
+    QSV_REQUIRE(st->n_local == prog->n_local, "qsv_program_run: state size differs from the program's");
+    qsv_ctx* ctx = st->ctx;
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    if (prog->has_collective || prog->steps.size() < 4)
+        return enqueue_steps(st, prog, nullptr);
+    auto it = prog->graphs.find(st->amps);
+    if (it == prog->graphs.end()) {
+        // First run on this buffer: run eagerly (configures kernel attributes),
+        // then capture the launch sequence as a CUDA graph for later runs.
+        int rc = enqueue_steps(st, prog, nullptr);
+        if (rc != QSV_OK)
+            return rc;
+        cudaGraph_t g = nullptr;
+        QSV_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_steps(st, prog, nullptr);
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+        if (rc != QSV_OK)
+            return rc;
+        QSV_CUDA(e);
+        cudaGraphExec_t ge = nullptr;
+        QSV_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        prog->graphs[st->amps] = ge;
+        return QSV_OK;
+    }
+    QSV_CUDA(cudaGraphLaunch(it->second, ctx->stream));
+    return QSV_OK;
+}
+
+extern "C" int qsv_program_profile(qsv_state* st, qsv_program* prog, float* ms_out) {
+    QSV_REQUIRE(st != nullptr && prog != nullptr && ms_out != nullptr, "qsv_program_profile: null argument");
+    qsv_ctx* ctx = st->ctx;
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    const size_t n = prog->steps.size();
+    std::vector<cudaEvent_t> evs(n + 1);
+    for (auto& e : evs)
+        QSV_CUDA(cudaEventCreate(&e));
+    int rc = enqueue_steps(st, prog, evs.data());
+    if (rc == QSV_OK) {
+        QSV_CUDA(cudaEventSynchronize(evs[n]));
+        for (size_t i = 0; i < n; ++i)
+            QSV_CUDA(cudaEventElapsedTime(&ms_out[i], evs[i], evs[i + 1]));
+    }
+    for (auto& e : evs)
+        cudaEventDestroy(e);
+    return rc;
+}
+
+extern "C" int qsv_program_step_cost(qsv_program* prog, int i, double* hbm_bytes, double* flops,
+                                     double* nvlink_bytes) {
+    QSV_REQUIRE(prog != nullptr && i >= 0 && i < static_cast<int>(prog->steps.size()),
+                "qsv_program_step_cost: bad step index");
+    const qsv::Step& s = prog->steps[i];
+    if (hbm_bytes) *hbm_bytes = s.hbm_bytes;
+    if (flops) *flops = s.flops;
+    if (nvlink_bytes) *nvlink_bytes = s.nvl_bytes;
+    return QSV_OK;
+}
+
+extern "C" int qsv_apply_fused(qsv_state* st, int k, const int* targets, uint64_t ctrl_mask,
+                               const double* mat) {
+    QSV_REQUIRE(st != nullptr && targets != nullptr && mat != nullptr, "qsv_apply_fused: null argument");
+    QSV_REQUIRE(k >= 1 && k <= QSV_MAX_DENSE_K, "qsv_apply_fused: k must be in [1, 5] (SPEC:89)");
+    qsv_ctx* ctx = st->ctx;
+    const int n_local = st->n_local;
+    const int n_total = n_local + log2i(ctx->nranks);
+    qsv_op_desc op{};
+    op.kind = QSV_OP_DENSE;
+    op.k = k;
+    for (int i = 0; i < k; ++i)
+        op.qubits[i] = targets[i];
+    op.ctrl_mask = ctrl_mask;
+    op.mat_off = 0;
+    // tile: low run plus the targets above it
+    qsv_step_desc sd{};
+    sd.kind = QSV_STEP_PASS;
+    const int K = std::min(10, n_local);
+    std::vector<int> high;
+    for (int i = 0; i < k; ++i)
+        if (targets[i] >= K - k)
+            high.push_back(targets[i]);
+    std::sort(high.begin(), high.end());
+    // shrink until the high set is consistent with the low run
+    int nh = static_cast<int>(high.size());
+    while (true) {
+        const int L = K - nh;
+        std::vector<int> hh;
+        for (int i = 0; i < k; ++i)
+            if (targets[i] >= L)
+                hh.push_back(targets[i]);
+        std::sort(hh.begin(), hh.end());
+        if (static_cast<int>(hh.size()) == nh) {
+            high = hh;
+            break;
+        }
+        nh = static_cast<int>(hh.size());
+    }
+    sd.tile_k = K;
+    sd.nhigh = static_cast<int>(high.size());
+    for (size_t i = 0; i < high.size(); ++i)
+        sd.high[i] = high[i];
+    sd.op_begin = 0;
+    sd.op_count = 1;
+    qsv_program* prog = nullptr;
+    int rc = qsv_program_create(ctx, n_total, n_local, &sd, 1, &op, 1, mat,
+                                static_cast<size_t>(1) << (2 * k), &prog);
+    if (rc != QSV_OK)
+        return rc;
+    rc = qsv_program_run(st, prog);
+    qsv_program_free(prog);
+    return rc;
+}
+
+// ======================================================================= reductions
+extern "C" int qsv_norm_sq(qsv_state* st, double* out) {
+    QSV_REQUIRE(st != nullptr && out != nullptr, "qsv_norm_sq: null argument");
+    qsv_ctx* ctx = st->ctx;
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    int rc = ensure_partials(ctx);
+    if (rc != QSV_OK)
+        return rc;
+    const int grid = reduce_grid(ctx);
+    norm_partial_kernel<<<grid, kRedThreads, 0, ctx->stream>>>(st->amps, st->size, ctx->d_partials);
+    QSV_CUDA(cudaGetLastError());
+    sum_partials_kernel<<<1, kRedThreads, 0, ctx->stream>>>(ctx->d_partials, grid,
+                                                           ctx->d_partials + ctx->partials_cap - 1);
+    QSV_CUDA(cudaGetLastError());
+    QSV_CUDA(cudaMemcpyAsync(ctx->h_result, ctx->d_partials + ctx->partials_cap - 1, sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    QSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = ctx->h_result[0];
+    return QSV_OK;
+}
+
+extern "C" int qsv_max_abs_diff(qsv_state* st, const double* host_ref, uint64_t offset, uint64_t count,
+                                double* out) {
+    QSV_REQUIRE(st != nullptr && out != nullptr && (host_ref != nullptr || count == 0),
+                "qsv_max_abs_diff: null argument");
+    QSV_REQUIRE(offset <= st->size && count <= st->size - offset, "qsv_max_abs_diff: range outside shard");
+    qsv_ctx* ctx = st->ctx;
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    int rc = ensure_partials(ctx);
+    if (rc != QSV_OK)
+        return rc;
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 26);  // 1 GiB staging at most
+    if (ctx->scratch_bytes < chunk * sizeof(double2)) {
+        if (ctx->d_scratch)
+            cudaFree(ctx->d_scratch);
+        ctx->d_scratch = nullptr;
+        ctx->scratch_bytes = 0;
+        QSV_CUDA(cudaMalloc(&ctx->d_scratch, std::max<uint64_t>(chunk, 1) * sizeof(double2)));
+        ctx->scratch_bytes = std::max<uint64_t>(chunk, 1) * sizeof(double2);
+    }
+    double worst = 0.0;
+    const int grid = reduce_grid(ctx);
+    for (uint64_t done = 0; done < count; done += chunk) {
+        const uint64_t c = std::min(chunk, count - done);
+        QSV_CUDA(cudaMemcpyAsync(ctx->d_scratch, host_ref + 2 * done, c * sizeof(double2),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        diff_partial_kernel<<<grid, kRedThreads, 0, ctx->stream>>>(
+            st->amps + offset + done, reinterpret_cast<const double2*>(ctx->d_scratch), c, ctx->d_partials);
+        QSV_CUDA(cudaGetLastError());
+        double m = 0.0;
+        rc = finish_max(ctx, grid, &m);
+        if (rc != QSV_OK)
+            return rc;
+        worst = std::max(worst, m);
+    }
+    *out = worst;
+    return QSV_OK;
+}
+
+extern "C" int qsv_check_qft_basis(qsv_state* st, int n_total, uint64_t x, double* out) {
+    QSV_REQUIRE(st != nullptr && out != nullptr, "qsv_check_qft_basis: null argument");
+    QSV_REQUIRE(n_total >= st->n_local && n_total <= QSV_MAX_QUBITS, "qsv_check_qft_basis: bad n_total");
+    qsv_ctx* ctx = st->ctx;
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    int rc = ensure_partials(ctx);
+    if (rc != QSV_OK)
+        return rc;
+    const int grid = reduce_grid(ctx);
+    qft_check_kernel<<<grid, kRedThreads, 0, ctx->stream>>>(
+        st->amps, st->size, static_cast<uint64_t>(ctx->rank) << st->n_local, n_total, x, ctx->d_partials);
+    QSV_CUDA(cudaGetLastError());
+    return finish_max(ctx, grid, out);
+}
+
+extern "C" int qsv_state_digest(qsv_state* st, uint64_t* out) {
+    QSV_REQUIRE(st != nullptr && out != nullptr, "qsv_state_digest: null argument");
+    qsv_ctx* ctx = st->ctx;
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    int rc = ensure_partials(ctx);
+    if (rc != QSV_OK)
+        return rc;
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(ctx->d_partials);
+    QSV_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), ctx->stream));
+    digest_kernel<<<reduce_grid(ctx), kRedThreads, 0, ctx->stream>>>(
+        reinterpret_cast<const unsigned long long*>(st->amps), 2 * st->size, d);
+    QSV_CUDA(cudaGetLastError());
+    QSV_CUDA(cudaMemcpyAsync(ctx->h_result, d, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    QSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    uint64_t w[2];
+    std::memcpy(w, ctx->h_result, sizeof(w));
+    *out = w[0] ^ (w[1] * 0xD6E8FEB86659FD93ull);
+    return QSV_OK;
+}
+
+extern "C" int qsv_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf) {
+    QSV_REQUIRE(st != nullptr, "qsv_swap: null state");
+    return qsv::run_swap(st, g, v, chunk_log2, nbuf);
+}
