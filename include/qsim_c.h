@@ -42,12 +42,12 @@ typedef struct qsim_plan_opts {
     int32_t multi_op_passes;  /* SMGP multi-block passes on (1) / off (0)       */
     int32_t chunk_log2;       /* BBOP batch 2^b amplitudes                      */
     int32_t nbuf;             /* BBOP buffers B                                 */
-    int32_t reserved;
+    int32_t register_blocks;  /* group native gates on <= 4 qubits (RBLOCK)     */
     double pass_budget;       /* DP cost units per amplitude per pass           */
 } qsim_plan_opts;
 
 typedef struct qsim_plan_stats {
-    int64_t gates_in, ops_lowered, ops_fused, passes, swaps;
+    int64_t gates_in, ops_lowered, ops_fused, ops_final, passes, swaps;
     double cost_units;
     int32_t max_dense_k, n, n_local, nsteps;
 } qsim_plan_stats;

@@ -111,6 +111,28 @@ int qsv_apply_fused(qsv_state* st, int k, const int* targets, uint64_t ctrl_mask
 #define QSV_OP_DENSE 0  /* dense 2^k matrix on k LOCAL targets (+ controls)          */
 #define QSV_OP_DIAG 1   /* diagonal of 2^k entries on k qubits (any, incl. global) */
 #define QSV_OP_XPERM 2  /* Pauli-X permutation on one LOCAL target (+ controls)    */
+#define QSV_OP_RBLOCK 3 /* register block: a list of primitives (U1/U2/CX/DIAG16) on
+                         * 4 LOCAL tile qubits qubits[0..3], applied to each 16-amplitude
+                         * group in registers (one SMEM round trip for the whole list) */
+#define QSV_OP_PHASEPROD 4 /* separable phase product: for amplitudes with all ctrl_mask
+                         * bits set, multiply by pool[mat_off] * prod over FACTOR
+                         * primitives (qubit q set) of pool[prim.mat_off]; qubits
+                         * anywhere (tile, out-of-tile, rank).  CP/CZ chains (QFT).   */
+
+/* Primitive kinds (RBLOCK: a, b index qubits[0..3] of the op; PHASEPROD: a is a
+ * physical qubit).  Matrices are complex, row-major, in the pool. */
+#define QSV_PRIM_U1 0      /* 2x2 on block qubit a                                   */
+#define QSV_PRIM_U2 1      /* 4x4 on block qubits (a, b), a < b, a = low matrix bit   */
+#define QSV_PRIM_CX 2      /* X on block qubit b controlled by block qubit a          */
+#define QSV_PRIM_DIAG16 3  /* 16-entry diagonal over the 4 block qubits (bit i = qubits[i]) */
+#define QSV_PRIM_FACTOR 4  /* PHASEPROD factor: multiply when physical qubit a is 1    */
+
+typedef struct qsv_prim_desc {
+    int32_t kind;
+    int32_t a, b;
+    int32_t pad;
+    int64_t mat_off;       /* complex offset into the pool                          */
+} qsv_prim_desc;
 
 typedef struct qsv_op_desc {
     int32_t kind;          /* QSV_OP_*                                              */
@@ -118,6 +140,8 @@ typedef struct qsv_op_desc {
     int32_t qubits[QSV_MAX_DIAG_K]; /* physical qubits; qubits[p] = bit p of the matrix index */
     uint64_t ctrl_mask;    /* physical GLOBAL index bits that must all be 1         */
     int64_t mat_off;       /* offset (complex entries) into the program's pool       */
+    int32_t prim_begin;    /* RBLOCK / PHASEPROD: primitives [prim_begin, +nprim)    */
+    int32_t nprim;
 } qsv_op_desc;
 
 /* Step kinds of a program. */
@@ -144,13 +168,15 @@ typedef struct qsv_step_desc {
 int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local,
                        const qsv_step_desc* steps, int nsteps,
                        const qsv_op_desc* ops, int nops,
+                       const qsv_prim_desc* prims, int nprims,
                        const double* pool, size_t pool_len, qsv_program** out);
 int qsv_program_free(qsv_program* prog);
 /* Host-only dry run of qsv_program_create's validation and tile compilation
  * (no device needed): returns QSV_OK iff the program would be accepted for
  * rank `rank`.  Used by CPU tests of the planner. */
 int qsv_program_validate(int n_total, int n_local, int rank, const qsv_step_desc* steps, int nsteps,
-                         const qsv_op_desc* ops, int nops, const double* pool, size_t pool_len);
+                         const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims, int nprims,
+                         const double* pool, size_t pool_len);
 /* Enqueues every step of the program on the context stream (a CUDA graph when
  * the program has no collective steps).  Replaces run_local and
  * run_distributed's dispatch loop. */

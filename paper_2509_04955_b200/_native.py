@@ -52,7 +52,7 @@ class qsim_plan_opts(C.Structure):
         ("multi_op_passes", C.c_int32),
         ("chunk_log2", C.c_int32),
         ("nbuf", C.c_int32),
-        ("reserved", C.c_int32),
+        ("register_blocks", C.c_int32),
         ("pass_budget", C.c_double),
     ]
 
@@ -62,6 +62,7 @@ class qsim_plan_stats(C.Structure):
         ("gates_in", C.c_int64),
         ("ops_lowered", C.c_int64),
         ("ops_fused", C.c_int64),
+        ("ops_final", C.c_int64),
         ("passes", C.c_int64),
         ("swaps", C.c_int64),
         ("cost_units", C.c_double),
@@ -128,26 +129,27 @@ def _dptr(a: np.ndarray):
 
 @dataclass
 class PlanOptions:
-    tile_k: int = 10
+    tile_k: int = 11
     min_low: int = 5
-    fuse_k: int = 3
+    fuse_k: int = 2
     fusion: bool = True
     multi_op_passes: bool = True
     chunk_log2: int = 22
     nbuf: int = 2
-    pass_budget: float = 64.0
+    pass_budget: float = 72.0
+    register_blocks: bool = True
 
     @classmethod
     def default(cls) -> "PlanOptions":
         o = qsim_plan_opts()
         load_qsim().qsim_default_opts(C.byref(o))
         return cls(o.tile_k, o.min_low, o.fuse_k, bool(o.fusion), bool(o.multi_op_passes),
-                   o.chunk_log2, o.nbuf, o.pass_budget)
+                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks))
 
     def to_c(self) -> qsim_plan_opts:
         return qsim_plan_opts(self.tile_k, self.min_low, self.fuse_k, int(self.fusion),
-                              int(self.multi_op_passes), self.chunk_log2, self.nbuf, 0,
-                              float(self.pass_budget))
+                              int(self.multi_op_passes), self.chunk_log2, self.nbuf,
+                              int(self.register_blocks), float(self.pass_budget))
 
 
 class Circuit:

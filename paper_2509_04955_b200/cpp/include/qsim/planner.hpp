@@ -28,26 +28,38 @@
 
 namespace qsim {
 
-enum class OpKind { Dense, Diag, XPerm, Fence };
+enum class OpKind { Dense, Diag, XPerm, PhaseProd, RBlock, Fence };
+
+// RBLOCK primitive (block-local qubit indices into Op::qubits).
+struct Prim {
+    int kind = QSV_PRIM_U1;     // QSV_PRIM_U1 / U2 / CX / DIAG16
+    int a = 0, b = 0;
+    std::vector<Amp> data;      // U1: 4, U2: 16, DIAG16: 16 entries
+};
 
 // One lowered op on LOGICAL qubits.
 struct Op {
     OpKind kind = OpKind::Dense;
-    std::vector<int> qubits;    // Dense/XPerm: targets; Diag: diagonal qubits (qubits[p] = bit p)
+    std::vector<int> qubits;    // Dense/XPerm: targets; Diag: diagonal qubits (qubits[p] = bit p);
+                                // RBlock: block qubits (<= 4)
     std::vector<int> controls;  // all must be 1
-    std::vector<Amp> data;      // Dense: 4^k entries row-major; Diag: 2^k entries
+    std::vector<Amp> data;      // Dense: 4^k entries row-major; Diag: 2^k entries;
+                                // PhaseProd: data[0] = constant factor
+    std::vector<std::pair<int, Amp>> factors;  // PhaseProd: multiply by f when qubit is 1
+    std::vector<Prim> prims;    // RBlock
     int first_gate = -1;        // provenance (gate index range)
     int last_gate = -1;
     int ngates = 0;             // source gates merged into this op
 };
 
 struct PlanOptions {
-    int tile_k = 10;          // tile qubits per pass (<= 11)
+    int tile_k = 11;          // tile qubits per pass (<= 11)
     int min_low = 5;          // contiguous low run: 2^5 amplitudes = 512-B DRAM runs
-    int fuse_k = 3;           // largest dense block fusion may create (<= QSV_MAX_DENSE_K)
+    int fuse_k = 2;           // largest dense block fusion may create (<= QSV_MAX_DENSE_K)
+    bool register_blocks = true;  // group native gates on <= 4 qubits into RBLOCK ops
     bool fusion = true;       // DAGC on/off (BASELINE configs[1]: "contraction on vs off")
     bool multi_op_passes = true;  // SMGP on/off: off = one op per pass
-    double pass_budget = 64;  // DP cost units per amplitude allowed in one pass
+    double pass_budget = 72;  // DP cost units per amplitude allowed in one pass
     int n_local = -1;         // local qubits per rank (-1: all, single GPU)
     int chunk_log2 = 22;      // BBOP batch: 2^b amplitudes per swap message
     int nbuf = 2;             // BBOP buffers B (default 2)
@@ -57,6 +69,7 @@ struct PlanStats {
     std::size_t gates_in = 0;      // gates excluding barriers (gates/s numerator)
     std::size_t ops_lowered = 0;
     std::size_t ops_fused = 0;     // ops after fusion
+    std::size_t ops_final = 0;     // ops after register blocking (what the kernels run)
     std::size_t passes = 0;
     std::size_t swaps = 0;
     double cost_units = 0;         // sum of op costs (DP units / amplitude)
@@ -68,6 +81,7 @@ struct Plan {
     int n_local = 0;
     std::vector<qsv_step_desc> steps;
     std::vector<qsv_op_desc> ops;
+    std::vector<qsv_prim_desc> prims;
     std::vector<double> pool;          // complex entries, re/im interleaved
     std::vector<Op> fused;             // fused ops (logical qubits), for inspection/tests
     PlanStats stats;
@@ -76,6 +90,8 @@ struct Plan {
 // Classification helpers.
 std::vector<Op> lower(const Circuit& c);
 std::vector<Op> fuse_ops(const std::vector<Op>& ops, const PlanOptions& opt);
+// Groups ops acting on <= 4 qubits into register blocks (RBLOCK).
+std::vector<Op> form_blocks(const std::vector<Op>& ops);
 // Relative DP cost per amplitude of one op (the packing / fusion currency).
 double op_cost(const Op& op);
 // Builds the full plan (lower -> fuse -> partition/swaps -> pack).

@@ -52,6 +52,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.fuse_k = o->fuse_k;
     p.fusion = o->fusion != 0;
     p.multi_op_passes = o->multi_op_passes != 0;
+    p.register_blocks = o->register_blocks != 0;
     p.chunk_log2 = o->chunk_log2;
     p.nbuf = o->nbuf;
     p.pass_budget = o->pass_budget;
@@ -62,6 +63,7 @@ void fill_stats(const qsim::Plan& p, qsim_plan_stats* s) {
     s->gates_in = static_cast<int64_t>(p.stats.gates_in);
     s->ops_lowered = static_cast<int64_t>(p.stats.ops_lowered);
     s->ops_fused = static_cast<int64_t>(p.stats.ops_fused);
+    s->ops_final = static_cast<int64_t>(p.stats.ops_final);
     s->passes = static_cast<int64_t>(p.stats.passes);
     s->swaps = static_cast<int64_t>(p.stats.swaps);
     s->cost_units = p.stats.cost_units;
@@ -101,6 +103,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->fuse_k = p.fuse_k;
     out->fusion = p.fusion;
     out->multi_op_passes = p.multi_op_passes;
+    out->register_blocks = p.register_blocks;
     out->chunk_log2 = p.chunk_log2;
     out->nbuf = p.nbuf;
     out->pass_budget = p.pass_budget;
@@ -213,6 +216,8 @@ int qsim_circuit_fused(const qsim_circuit* c, const qsim_plan_opts* opts, qsim_c
         std::vector<qsim::Op> ops = qsim::lower(c->c);
         if (o.fusion) {
             ops = qsim::fuse_ops(ops, o);
+            if (o.register_blocks)
+                ops = qsim::form_blocks(ops);
         }
         std::vector<qsim::Op> kept;
         for (auto& op : ops)
@@ -232,7 +237,8 @@ int qsim_circuit_plan(const qsim_circuit* c, const qsim_plan_opts* opts, int n_l
         const qsim::Plan p = qsim::make_plan(c->c, o);
         const int rc = qsv_program_validate(p.n, p.n_local, rank, p.steps.data(),
                                             static_cast<int>(p.steps.size()), p.ops.data(),
-                                            static_cast<int>(p.ops.size()), p.pool.data(), p.pool.size() / 2);
+                                            static_cast<int>(p.ops.size()), p.prims.data(),
+                                            static_cast<int>(p.prims.size()), p.pool.data(), p.pool.size() / 2);
         if (rc != QSV_OK) {
             t_err = std::string("plan rejected by the device compiler: ") + qsv_last_error();
             return rc;

@@ -76,7 +76,8 @@ Engine::Engine(DeviceContext& ctx, const Circuit& c, const PlanOptions& opt) : c
     plan_ = make_plan(c, o);
     qsv_check(qsv_program_create(ctx.get(), plan_.n, plan_.n_local, plan_.steps.data(),
                                  static_cast<int>(plan_.steps.size()), plan_.ops.data(),
-                                 static_cast<int>(plan_.ops.size()), plan_.pool.data(),
+                                 static_cast<int>(plan_.ops.size()), plan_.prims.data(),
+                                 static_cast<int>(plan_.prims.size()), plan_.pool.data(),
                                  plan_.pool.size() / 2, &prog_),
               "qsv_program_create");
 }

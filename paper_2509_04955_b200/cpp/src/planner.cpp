@@ -4,11 +4,24 @@
 #include <algorithm>
 #include <cmath>
 #include <limits>
+#include <map>
+#include <optional>
 #include <stdexcept>
 
 namespace qsim {
 
 namespace {
+
+using Factors = std::vector<std::pair<int, Amp>>;
+
+bool contains(const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(), x) != v.end(); }
+
+int index_of(const std::vector<int>& v, int x) {
+    for (std::size_t i = 0; i < v.size(); ++i)
+        if (v[i] == x)
+            return static_cast<int>(i);
+    return -1;
+}
 
 bool matrix_is_diagonal(const GateMatrix& m) {
     const Index d = m.dim();
@@ -24,27 +37,52 @@ bool matrix_is_x(const GateMatrix& m) {
            m.at(0, 1) == Amp{1.0, 0.0} && m.at(1, 0) == Amp{1.0, 0.0};
 }
 
-std::vector<int> all_qubits(const Op& o) {
+bool diag_like(const Op& o) { return o.kind == OpKind::Diag || o.kind == OpKind::PhaseProd; }
+
+// Every qubit an op reads or writes (its DAG footprint).
+std::vector<int> footprint(const Op& o) {
     std::vector<int> q = o.qubits;
-    q.insert(q.end(), o.controls.begin(), o.controls.end());
+    for (int c : o.controls)
+        if (!contains(q, c))
+            q.push_back(c);
+    for (const auto& f : o.factors)
+        if (!contains(q, f.first))
+            q.push_back(f.first);
     return q;
 }
 
-bool contains(const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(), x) != v.end(); }
-
-int index_of(const std::vector<int>& v, int x) {
-    for (std::size_t i = 0; i < v.size(); ++i)
-        if (v[i] == x)
-            return static_cast<int>(i);
-    return -1;
+// Diagonal value of a diag-like op on a basis state given by bit(q).
+template <typename Bit>
+Amp diag_value(const Op& o, Bit&& bit) {
+    for (int c : o.controls)
+        if (!bit(c))
+            return Amp{1.0, 0.0};
+    if (o.kind == OpKind::Diag) {
+        std::size_t lin = 0;
+        for (std::size_t i = 0; i < o.qubits.size(); ++i)
+            lin |= static_cast<std::size_t>(bit(o.qubits[i])) << i;
+        return o.data[lin];
+    }
+    Amp v = o.data[0];
+    for (const auto& f : o.factors)
+        if (bit(f.first))
+            v *= f.second;
+    return v;
 }
 
 // Dense matrix (2^|T| x 2^|T|, row-major) of `op` acting on the ordered qubit
 // list T (bit p <-> T[p]) inside the subspace where the controls NOT in T are 1.
-// Requires op.qubits within T; op.controls within T or within the kept controls.
 std::vector<Amp> expand_dense(const Op& op, const std::vector<int>& T) {
     const std::size_t D = std::size_t{1} << T.size();
     std::vector<Amp> out(D * D, Amp{0.0, 0.0});
+    if (diag_like(op)) {
+        for (std::size_t j = 0; j < D; ++j)
+            out[j * D + j] = diag_value(op, [&](int q) {
+                const int p = index_of(T, q);
+                return p < 0 ? 1 : static_cast<int>((j >> p) & 1);
+            });
+        return out;
+    }
     std::vector<int> p(op.qubits.size());
     std::size_t opmask = 0;
     for (std::size_t i = 0; i < op.qubits.size(); ++i) {
@@ -68,23 +106,17 @@ std::vector<Amp> expand_dense(const Op& op, const std::vector<int>& T) {
         for (std::size_t i = 0; i < k; ++i)
             lin |= ((j >> p[i]) & 1) << i;
         const std::size_t rest = j & ~opmask;
-        switch (op.kind) {
-        case OpKind::Dense:
+        if (op.kind == OpKind::Dense) {
             for (std::size_t rl = 0; rl < dk; ++rl) {
                 std::size_t row = rest;
                 for (std::size_t i = 0; i < k; ++i)
                     row |= ((rl >> i) & 1) << p[i];
                 out[row * D + j] = op.data[rl * dk + lin];
             }
-            break;
-        case OpKind::Diag:
-            out[j * D + j] = op.data[lin];
-            break;
-        case OpKind::XPerm:
+        } else if (op.kind == OpKind::XPerm) {
             out[(j ^ (std::size_t{1} << p[0])) * D + j] = Amp{1.0, 0.0};
-            break;
-        case OpKind::Fence:
-            throw std::logic_error("expand_dense: fence");
+        } else {
+            throw std::logic_error("expand_dense: unsupported op kind");
         }
     }
     return out;
@@ -118,21 +150,100 @@ void canonical_phase(Op& o) {
     o.data.assign(1, last);
 }
 
-// Merge B (later) into A (earlier); returns false when the result would exceed
-// the arity limits.
+// Re-express a diag-like op as a phase product controlled by exactly C.
+std::optional<std::pair<Factors, Amp>> as_phaseprod(const Op& o, const std::vector<int>& C) {
+    std::vector<int> own = o.controls;
+    for (int c : C)
+        if (!contains(own, c))
+            return std::nullopt;  // C must be a subset of the op's controls
+    std::vector<int> extra;
+    for (int c : own)
+        if (!contains(C, c))
+            extra.push_back(c);
+    Factors f;
+    Amp c0{1.0, 0.0};
+    if (o.kind == OpKind::PhaseProd) {
+        f = o.factors;
+        c0 = o.data[0];
+    } else if (o.qubits.empty()) {
+        c0 = o.data[0];
+    } else if (o.qubits.size() == 1 && o.data[0] != Amp{0.0, 0.0}) {
+        c0 = o.data[0];
+        f.push_back({o.qubits[0], o.data[1] / o.data[0]});
+    } else {
+        return std::nullopt;
+    }
+    if (extra.size() > 1)
+        return std::nullopt;
+    if (extra.size() == 1) {
+        if (!f.empty())
+            return std::nullopt;  // c0 * prod f under an extra control is not separable
+        f.push_back({extra[0], c0});
+        c0 = Amp{1.0, 0.0};
+    }
+    return std::make_pair(f, c0);
+}
+
+Op make_phaseprod(const Op& A, const Op& B, const std::vector<int>& C, const Factors& fa, Amp ca,
+                  const Factors& fb, Amp cb) {
+    Op out;
+    out.kind = OpKind::PhaseProd;
+    out.controls = C;
+    std::map<int, Amp> acc;
+    for (const auto* fs : {&fa, &fb})
+        for (const auto& f : *fs) {
+            auto it = acc.find(f.first);
+            if (it == acc.end())
+                acc[f.first] = f.second;
+            else
+                it->second *= f.second;
+        }
+    for (const auto& kv : acc)
+        if (!contains(C, kv.first))
+            out.factors.push_back(kv);
+    Amp c = ca * cb;
+    for (const auto& kv : acc)
+        if (contains(C, kv.first))
+            c *= kv.second;  // a factor on a control qubit is always applied
+    out.data = {c};
+    out.first_gate = std::min(A.first_gate, B.first_gate);
+    out.last_gate = std::max(A.last_gate, B.last_gate);
+    out.ngates = A.ngates + B.ngates;
+    return out;
+}
+
+// Merge B (later) into A (earlier); false when no legal/within-limit merge exists.
 bool merge_ops(const Op& A, const Op& B, int fuse_k, Op& out) {
+    if (A.kind == OpKind::Fence || B.kind == OpKind::Fence || A.kind == OpKind::RBlock ||
+        B.kind == OpKind::RBlock)
+        return false;
+    if (diag_like(A) && diag_like(B)) {
+        // (1) separable phase product under the common controls
+        std::vector<int> C;
+        for (int c : A.controls)
+            if (contains(B.controls, c))
+                C.push_back(c);
+        std::sort(C.begin(), C.end());
+        const auto pa = as_phaseprod(A, C);
+        const auto pb = as_phaseprod(B, C);
+        if (pa && pb) {
+            out = make_phaseprod(A, B, C, pa->first, pa->second, pb->first, pb->second);
+            return true;
+        }
+    }
     std::vector<int> C;  // controls common to both stay controls
-    for (int c : A.controls)
-        if (contains(B.controls, c))
-            C.push_back(c);
+    if (A.kind != OpKind::PhaseProd && B.kind != OpKind::PhaseProd)
+        for (int c : A.controls)
+            if (contains(B.controls, c))
+                C.push_back(c);
     std::vector<int> T;
     for (const Op* o : {&A, &B})
-        for (int q : all_qubits(*o))
+        for (int q : footprint(*o))
             if (!contains(C, q) && !contains(T, q))
                 T.push_back(q);
     std::sort(T.begin(), T.end());
     std::sort(C.begin(), C.end());
-    const bool both_diag = A.kind == OpKind::Diag && B.kind == OpKind::Diag;
+    const bool both_diag = diag_like(A) && diag_like(B);
     const int limit = both_diag ? QSV_MAX_DIAG_K : fuse_k;
     if (static_cast<int>(T.size()) > limit)
         return false;
@@ -147,26 +258,13 @@ bool merge_ops(const Op& A, const Op& B, int fuse_k, Op& out) {
     out.ngates = A.ngates + B.ngates;
     if (both_diag) {
         out.kind = OpKind::Diag;
-        out.data.assign(D, Amp{1.0, 0.0});
-        for (const Op* o : {&A, &B}) {
-            // diagonal entry of o at T-pattern e
-            std::vector<int> p(o->qubits.size());
-            for (std::size_t i = 0; i < p.size(); ++i)
-                p[i] = index_of(T, o->qubits[i]);
-            std::size_t cm = 0;
-            for (int c : o->controls) {
-                const int pc = index_of(T, c);
-                if (pc >= 0)
-                    cm |= std::size_t{1} << pc;
-            }
-            for (std::size_t e = 0; e < D; ++e) {
-                if ((e & cm) != cm)
-                    continue;
-                std::size_t lin = 0;
-                for (std::size_t i = 0; i < p.size(); ++i)
-                    lin |= ((e >> p[i]) & 1) << i;
-                out.data[e] = o->data[lin] * out.data[e];
-            }
+        out.data.resize(D);
+        for (std::size_t e = 0; e < D; ++e) {
+            auto bit = [&](int q) {
+                const int p = index_of(T, q);
+                return p < 0 ? 1 : static_cast<int>((e >> p) & 1);
+            };
+            out.data[e] = diag_value(B, bit) * diag_value(A, bit);
         }
         canonical_phase(out);
         return true;
@@ -177,19 +275,89 @@ bool merge_ops(const Op& A, const Op& B, int fuse_k, Op& out) {
 }
 
 bool is_identity(const Op& o) {
-    if (o.kind == OpKind::XPerm || o.kind == OpKind::Fence)
+    if (o.kind == OpKind::XPerm || o.kind == OpKind::Fence || o.kind == OpKind::RBlock)
         return false;
-    const std::size_t D = o.kind == OpKind::Dense ? std::size_t{1} << o.qubits.size() : o.data.size();
-    for (std::size_t r = 0; r < D; ++r) {
-        if (o.kind == OpKind::Diag) {
-            if (o.data[r] != Amp{1.0, 0.0}) return false;
-            continue;
-        }
+    if (o.kind == OpKind::PhaseProd) {
+        if (o.data[0] != Amp{1.0, 0.0})
+            return false;
+        for (const auto& f : o.factors)
+            if (f.second != Amp{1.0, 0.0})
+                return false;
+        return true;
+    }
+    if (o.kind == OpKind::Diag) {
+        for (const Amp& a : o.data)
+            if (a != Amp{1.0, 0.0})
+                return false;
+        return true;
+    }
+    const std::size_t D = std::size_t{1} << o.qubits.size();
+    for (std::size_t r = 0; r < D; ++r)
         for (std::size_t c = 0; c < D; ++c)
             if (o.data[r * D + c] != (r == c ? Amp{1.0, 0.0} : Amp{0.0, 0.0}))
                 return false;
-    }
     return true;
+}
+
+// ------------------------------------------------------------ register blocks
+bool block_eligible(const Op& o) {
+    switch (o.kind) {
+    case OpKind::Dense: return o.qubits.size() + o.controls.size() <= 2;
+    case OpKind::XPerm: return o.controls.size() <= 1;
+    case OpKind::Diag:
+    case OpKind::PhaseProd: return footprint(o).size() <= 4;
+    default: return false;
+    }
+}
+
+double prim_cost(const Prim& p) {
+    switch (p.kind) {
+    case QSV_PRIM_U1: return 8.0;
+    case QSV_PRIM_U2: return 16.0;
+    case QSV_PRIM_CX: return 0.5;
+    default: return 4.0;
+    }
+}
+
+// Converts the member ops of a block (qubits sorted = slots) into primitives.
+std::vector<Prim> block_prims(const std::vector<int>& slots, const std::vector<Op>& members) {
+    std::vector<Prim> out;
+    auto slot = [&](int q) { return index_of(slots, q); };
+    for (const Op& o : members) {
+        Prim p;
+        if (diag_like(o)) {
+            p.kind = QSV_PRIM_DIAG16;
+            p.data.resize(16);
+            for (int e = 0; e < 16; ++e)
+                p.data[e] = diag_value(o, [&](int q) { return (e >> slot(q)) & 1; });
+            if (!out.empty() && out.back().kind == QSV_PRIM_DIAG16) {
+                for (int e = 0; e < 16; ++e)
+                    out.back().data[e] = p.data[e] * out.back().data[e];
+                continue;
+            }
+        } else if (o.kind == OpKind::XPerm && o.controls.size() == 1) {
+            p.kind = QSV_PRIM_CX;
+            p.a = slot(o.controls[0]);
+            p.b = slot(o.qubits[0]);
+        } else if (footprint(o).size() == 1) {
+            p.kind = QSV_PRIM_U1;
+            p.a = slot(o.qubits[0]);
+            p.data = expand_dense(o, {o.qubits[0]});
+            if (!out.empty() && out.back().kind == QSV_PRIM_U1 && out.back().a == p.a) {
+                out.back().data = matmul(p.data, out.back().data, 2);
+                continue;
+            }
+        } else {
+            std::vector<int> fp = footprint(o);
+            std::sort(fp.begin(), fp.end());
+            p.kind = QSV_PRIM_U2;
+            p.a = slot(fp[0]);
+            p.b = slot(fp[1]);
+            p.data = expand_dense(o, fp);
+        }
+        out.push_back(std::move(p));
+    }
+    return out;
 }
 
 } // namespace
@@ -197,9 +365,16 @@ bool is_identity(const Op& o) {
 double op_cost(const Op& o) {
     const double ctl = std::ldexp(1.0, -static_cast<int>(o.controls.size()));
     switch (o.kind) {
-    case OpKind::Dense: return 4.0 * std::ldexp(1.0, static_cast<int>(o.qubits.size())) * ctl + 2.0;
-    case OpKind::Diag: return 4.0 * ctl + 2.0;
-    case OpKind::XPerm: return 1.0 * ctl + 1.0;
+    case OpKind::Dense: return 4.0 * std::ldexp(1.0, static_cast<int>(o.qubits.size())) * ctl + 3.0;
+    case OpKind::Diag: return 4.0 * ctl + 3.0;
+    case OpKind::PhaseProd: return 8.0 * ctl + 3.0;
+    case OpKind::XPerm: return 1.0 * ctl + 2.0;
+    case OpKind::RBlock: {
+        double c = 3.0;
+        for (const Prim& p : o.prims)
+            c += prim_cost(p);
+        return c;
+    }
     case OpKind::Fence: return 0.0;
     }
     return 0.0;
@@ -244,11 +419,11 @@ std::vector<Op> fuse_ops(const std::vector<Op>& in, const PlanOptions& opt) {
     out.reserve(in.size());
     int nq = 0;
     for (const Op& o : in)
-        for (int q : all_qubits(o))
+        for (int q : footprint(o))
             nq = std::max(nq, q + 1);
     std::vector<int> frontier(static_cast<std::size_t>(nq), -1);
     for (const Op& b : in) {
-        const std::vector<int> qb = all_qubits(b);
+        const std::vector<int> qb = footprint(b);
         int a = -1;
         for (int q : qb)
             a = std::max(a, frontier[q]);
@@ -257,7 +432,7 @@ std::vector<Op> fuse_ops(const std::vector<Op>& in, const PlanOptions& opt) {
             if (merge_ops(out[a], b, opt.fuse_k, merged) &&
                 op_cost(merged) <= op_cost(out[a]) + op_cost(b) + 1e-9) {
                 out[a] = std::move(merged);
-                for (int q : all_qubits(out[a]))
+                for (int q : footprint(out[a]))
                     frontier[q] = std::max(frontier[q], a);
                 continue;
             }
@@ -276,6 +451,71 @@ std::vector<Op> fuse_ops(const std::vector<Op>& in, const PlanOptions& opt) {
     return kept;
 }
 
+std::vector<Op> form_blocks(const std::vector<Op>& in) {
+    struct Slot {
+        Op op;                    // the op (or the first member while a block is open)
+        std::vector<int> qubits;  // block footprint
+        std::vector<Op> members;  // > 1 when it became a block
+    };
+    std::vector<Slot> out;
+    int nq = 0;
+    for (const Op& o : in)
+        for (int q : footprint(o))
+            nq = std::max(nq, q + 1);
+    std::vector<int> frontier(static_cast<std::size_t>(nq), -1);
+    for (const Op& b : in) {
+        const std::vector<int> qb = footprint(b);
+        if (block_eligible(b)) {
+            int a = -1;
+            for (int q : qb)
+                a = std::max(a, frontier[q]);
+            if (a >= 0 && !out[a].members.empty()) {
+                std::vector<int> u = out[a].qubits;
+                for (int q : qb)
+                    if (!contains(u, q))
+                        u.push_back(q);
+                if (u.size() <= 4) {
+                    out[a].qubits = u;
+                    out[a].members.push_back(b);
+                    for (int q : u)
+                        frontier[q] = std::max(frontier[q], a);
+                    continue;
+                }
+            }
+            Slot s;
+            s.op = b;
+            s.qubits = qb;
+            s.members.push_back(b);
+            out.push_back(std::move(s));
+        } else {
+            Slot s;
+            s.op = b;
+            out.push_back(std::move(s));
+        }
+        for (int q : qb)
+            frontier[q] = static_cast<int>(out.size()) - 1;
+    }
+    std::vector<Op> res;
+    res.reserve(out.size());
+    for (Slot& s : out) {
+        if (s.members.size() <= 1) {
+            res.push_back(std::move(s.op));
+            continue;
+        }
+        Op blk;
+        blk.kind = OpKind::RBlock;
+        blk.qubits = s.qubits;
+        std::sort(blk.qubits.begin(), blk.qubits.end());
+        blk.prims = block_prims(blk.qubits, s.members);
+        blk.first_gate = s.members.front().first_gate;
+        blk.last_gate = s.members.back().last_gate;
+        for (const Op& m : s.members)
+            blk.ngates += m.ngates;
+        res.push_back(std::move(blk));
+    }
+    return res;
+}
+
 namespace {
 
 struct Packer {
@@ -284,7 +524,7 @@ struct Packer {
     Plan& plan;
     std::vector<int> pos;          // logical -> physical
     // current pass
-    std::vector<int> targets;      // physical dense/xperm targets in the pass
+    std::vector<int> targets;      // physical tile-resident targets of the pass
     std::vector<qsv_op_desc> cur_ops;
     double cur_cost = 0;
     std::size_t cur_bytes = 0;
@@ -323,7 +563,6 @@ struct Packer {
         for (int q : targets)
             if (q >= L)
                 high.push_back(q);
-        std::sort(high.begin(), high.end());
         // pad the tile with high qubits when targets don't fill it (K - L slots)
         const int want_high = K - L;
         for (int q = n_local - 1; static_cast<int>(high.size()) < want_high && q >= L; --q)
@@ -344,40 +583,125 @@ struct Packer {
         cur_bytes = 0;
     }
 
-    qsv_op_desc to_desc(const Op& o) {
-        qsv_op_desc d{};
-        d.k = static_cast<int>(o.qubits.size());
-        for (std::size_t i = 0; i < o.qubits.size(); ++i)
-            d.qubits[i] = pos[o.qubits[i]];
-        for (int c : o.controls)
-            d.ctrl_mask |= 1ull << pos[c];
-        d.kind = o.kind == OpKind::Dense ? QSV_OP_DENSE : (o.kind == OpKind::Diag ? QSV_OP_DIAG : QSV_OP_XPERM);
-        d.mat_off = static_cast<int64_t>(plan.pool.size() / 2);
-        for (const Amp& a : o.data) {
+    int64_t put(const std::vector<Amp>& d) {
+        const int64_t off = static_cast<int64_t>(plan.pool.size() / 2);
+        for (const Amp& a : d) {
             plan.pool.push_back(a.real());
             plan.pool.push_back(a.imag());
+        }
+        return off;
+    }
+
+    // Physical slots of a register block: its qubits plus low-run padding.
+    std::vector<int> block_slots(const Op& o) const {
+        std::vector<int> phys;
+        for (int q : o.qubits)
+            phys.push_back(pos[q]);
+        for (int p = 0; phys.size() < 4 && p < Lmin; ++p)
+            if (!contains(phys, p))
+                phys.push_back(p);
+        return phys;
+    }
+
+    // physical positions the op needs inside the tile
+    std::vector<int> tile_needs(const Op& o) const {
+        if (o.kind == OpKind::Dense || o.kind == OpKind::XPerm) {
+            std::vector<int> t;
+            for (int q : o.qubits)
+                t.push_back(pos[q]);
+            return t;
+        }
+        if (o.kind == OpKind::RBlock)
+            return block_slots(o);
+        return {};
+    }
+
+    qsv_op_desc to_desc(const Op& o) {
+        qsv_op_desc d{};
+        for (int c : o.controls)
+            d.ctrl_mask |= 1ull << pos[c];
+        switch (o.kind) {
+        case OpKind::Dense:
+        case OpKind::XPerm:
+        case OpKind::Diag:
+            d.kind = o.kind == OpKind::Dense ? QSV_OP_DENSE : (o.kind == OpKind::Diag ? QSV_OP_DIAG : QSV_OP_XPERM);
+            d.k = static_cast<int>(o.qubits.size());
+            for (std::size_t i = 0; i < o.qubits.size(); ++i)
+                d.qubits[i] = pos[o.qubits[i]];
+            d.mat_off = put(o.data);
+            break;
+        case OpKind::PhaseProd:
+            d.kind = QSV_OP_PHASEPROD;
+            d.k = 0;
+            d.mat_off = put(o.data);
+            d.prim_begin = static_cast<int>(plan.prims.size());
+            for (const auto& f : o.factors) {
+                qsv_prim_desc p{};
+                p.kind = QSV_PRIM_FACTOR;
+                p.a = pos[f.first];
+                p.mat_off = put({f.second});
+                plan.prims.push_back(p);
+            }
+            d.nprim = static_cast<int>(o.factors.size());
+            break;
+        case OpKind::RBlock: {
+            d.kind = QSV_OP_RBLOCK;
+            d.k = 4;
+            const std::vector<int> phys = block_slots(o);
+            for (int i = 0; i < 4; ++i)
+                d.qubits[i] = phys[i];
+            d.prim_begin = static_cast<int>(plan.prims.size());
+            // slot data is laid out over the block's own qubits (slots 0..|q|-1);
+            // padded slots are untouched qubits, so DIAG16 entries just repeat.
+            for (const Prim& pr : o.prims) {
+                qsv_prim_desc p{};
+                p.kind = pr.kind;
+                p.a = pr.a;
+                p.b = pr.b;
+                if (pr.kind == QSV_PRIM_DIAG16) {
+                    std::vector<Amp> t(16);
+                    const int nb = static_cast<int>(o.qubits.size());
+                    for (int e = 0; e < 16; ++e)
+                        t[e] = pr.data[e & ((1 << nb) - 1)];
+                    p.mat_off = put(t);
+                } else if (!pr.data.empty()) {
+                    p.mat_off = put(pr.data);
+                }
+                plan.prims.push_back(p);
+            }
+            d.nprim = static_cast<int>(o.prims.size());
+            break;
+        }
+        case OpKind::Fence:
+            throw std::logic_error("to_desc: fence");
         }
         return d;
     }
 
     static std::size_t blob_bytes(const Op& o) {
-        // TileOp record + member offsets + matrix/table, 16-B aligned pieces
         std::size_t b = 96;
-        if (o.kind == OpKind::Dense) {
+        switch (o.kind) {
+        case OpKind::Dense: {
             const std::size_t D = std::size_t{1} << o.qubits.size();
             b += ((D * 4 + 15) & ~std::size_t{15}) + D * D * 16;
-        } else if (o.kind == OpKind::Diag) {
-            b += o.data.size() * 16;
+            break;
+        }
+        case OpKind::Diag: b += o.data.size() * 16 + 96; break;
+        case OpKind::PhaseProd: b += 97 * 16 + o.factors.size() * 32; break;
+        case OpKind::RBlock:
+            for (const Prim& p : o.prims)
+                b += 8 + (p.kind == QSV_PRIM_U1 ? 64 : (p.kind == QSV_PRIM_CX ? 0 : 256)) + 16;
+            break;
+        default: break;
         }
         return b;
     }
 
     void add(const Op& o) {
         std::vector<int> need = targets;
-        if (o.kind == OpKind::Dense || o.kind == OpKind::XPerm)
-            for (int q : o.qubits)
-                if (!contains(need, pos[q]))
-                    need.push_back(pos[q]);
+        for (int p : tile_needs(o))
+            if (!contains(need, p))
+                need.push_back(p);
         const double c = op_cost(o);
         const std::size_t b = blob_bytes(o);
         const bool fits = low_run(need) >= 0 && (cur_ops.empty() || cur_cost + c <= opt.pass_budget) &&
@@ -389,6 +713,8 @@ struct Packer {
         }
         if (low_run(need) < 0)
             throw std::logic_error("planner: op does not fit a tile (k too large for tile_k)");
+        if (b > 36 * 1024)
+            throw std::logic_error("planner: op too large for one pass");
         targets = need;
         cur_ops.push_back(to_desc(o));
         cur_cost += c;
@@ -413,6 +739,13 @@ struct Packer {
         std::swap(pos[lg], pos[lv]);
     }
 };
+
+// logical qubits an op needs local (inside the tile)
+std::vector<int> local_needs(const Op& o) {
+    if (o.kind == OpKind::Dense || o.kind == OpKind::XPerm || o.kind == OpKind::RBlock)
+        return o.qubits;
+    return {};
+}
 
 } // namespace
 
@@ -440,6 +773,10 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
         ops = std::move(kept);
     }
     plan.stats.ops_fused = ops.size();
+    const int K = std::min(opt.tile_k, plan.n_local);
+    if (opt.fusion && opt.register_blocks && K >= std::max(opt.min_low, 5) && opt.multi_op_passes)
+        ops = form_blocks(ops);
+    plan.stats.ops_final = ops.size();
     for (const Op& o : ops) {
         plan.stats.cost_units += op_cost(o);
         if (o.kind == OpKind::Dense)
@@ -447,17 +784,12 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     }
 
     Packer pk(opt, c.n, plan.n_local, plan);
-    // next-use table for victim selection: for each op index, when is logical q
-    // next needed as a dense/xperm target?
+    // next tile use of each logical qubit, for swap-victim selection (Belady)
     const int nops = static_cast<int>(ops.size());
-    auto needs_tile = [](const Op& o, int q) {
-        return (o.kind == OpKind::Dense || o.kind == OpKind::XPerm) && contains(o.qubits, q);
-    };
     std::vector<std::vector<int>> uses(c.n);
     for (int i = 0; i < nops; ++i)
-        for (int q : ops[i].qubits)
-            if (needs_tile(ops[i], q))
-                uses[q].push_back(i);
+        for (int q : local_needs(ops[i]))
+            uses[q].push_back(i);
     std::vector<std::size_t> cursor(c.n, 0);
     auto next_use = [&](int q, int from) {
         auto& u = uses[q];
@@ -468,31 +800,26 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     };
     for (int i = 0; i < nops; ++i) {
         const Op& o = ops[i];
-        if (o.kind == OpKind::Dense || o.kind == OpKind::XPerm) {
-            for (int q : o.qubits) {
-                if (pk.pos[q] < plan.n_local)
+        const std::vector<int> need = local_needs(o);
+        for (int q : need) {
+            if (pk.pos[q] < plan.n_local)
+                continue;
+            int best = -1;
+            long long best_score = -1;
+            for (int l = 0; l < c.n; ++l) {
+                const int p = pk.pos[l];
+                if (p >= plan.n_local || contains(need, l) || p < pk.Lmin)
                     continue;
-                // choose the local victim whose next tile use is farthest away,
-                // preferring high physical positions (contiguous swap chunks)
-                int best = -1;
-                long long best_score = -1;
-                for (int l = 0; l < c.n; ++l) {
-                    const int p = pk.pos[l];
-                    if (p >= plan.n_local || contains(o.qubits, l))
-                        continue;
-                    if (contains(pk.targets, p))
-                        continue;
-                    const long long nu = next_use(l, i);
-                    const long long score = nu * 64 + p;
-                    if (score > best_score) {
-                        best_score = score;
-                        best = l;
-                    }
+                const long long nu = next_use(l, i);
+                const long long score = nu * 64 + p;
+                if (score > best_score) {
+                    best_score = score;
+                    best = l;
                 }
-                if (best < 0)
-                    throw std::logic_error("planner: no swap victim available");
-                pk.swap(pk.pos[q], pk.pos[best]);
             }
+            if (best < 0)
+                throw std::logic_error("planner: no swap victim available");
+            pk.swap(pk.pos[q], pk.pos[best]);
         }
         pk.add(o);
     }
@@ -501,26 +828,23 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     for (int q = 0; q < c.n; ++q) {
         if (pk.pos[q] == q)
             continue;
-        // q sits at pos[q]; whoever sits at q must move. One swap per global slot.
         int other = -1;
         for (int r = 0; r < c.n; ++r)
             if (pk.pos[r] == q)
                 other = r;
         const int a = pk.pos[q], b = q;  // physical slots to exchange
-        if (a >= plan.n_local && b < plan.n_local)
+        if (a >= plan.n_local && b < plan.n_local) {
             pk.swap(a, b);
-        else if (b >= plan.n_local && a < plan.n_local)
+        } else if (b >= plan.n_local && a < plan.n_local) {
             pk.swap(b, a);
-        else if (a < plan.n_local && b < plan.n_local) {
-            // local-local relabel: a SWAP of two local qubits as one dense pass
+        } else if (a < plan.n_local && b < plan.n_local) {
+            // local-local relabel: a SWAP of the two physical slots as one dense op
             Op sw;
             sw.kind = OpKind::Dense;
             sw.qubits = {q, other};
             sw.data.assign(16, Amp{0.0, 0.0});
             sw.data[0] = sw.data[15] = Amp{1.0, 0.0};
             sw.data[1 * 4 + 2] = sw.data[2 * 4 + 1] = Amp{1.0, 0.0};
-            // pos[] maps logical->physical: the op must act on the physical
-            // slots a and b, and afterwards q sits at b and other at a.
             pk.add(sw);
             pk.close_pass();
             std::swap(pk.pos[q], pk.pos[other]);
@@ -538,29 +862,64 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
 
 Circuit ops_to_circuit(int n, const std::vector<Op>& ops) {
     Circuit c(n, "fused");
-    for (const Op& o : ops) {
-        if (o.kind == OpKind::Fence)
-            continue;
-        std::vector<int> t = o.qubits, ctl = o.controls;
-        std::vector<Amp> m;
-        int k = static_cast<int>(t.size());
-        if (o.kind == OpKind::Dense) {
-            m = o.data;
-        } else if (o.kind == OpKind::XPerm) {
-            m = {0.0, 1.0, 1.0, 0.0};
-        } else if (k == 0) {
-            // phase on all-ones of the controls: diag(1, e) on the last control
-            t = {ctl.back()};
-            ctl.pop_back();
-            m = {1.0, 0.0, 0.0, o.data[0]};
-            k = 1;
-        } else {
-            const std::size_t D = o.data.size();
-            m.assign(D * D, Amp{0.0, 0.0});
-            for (std::size_t i = 0; i < D; ++i)
-                m[i * D + i] = o.data[i];
+    auto add_matrix = [&](std::vector<int> t, std::vector<int> ctl, std::vector<Amp> m) {
+        const int k = static_cast<int>(t.size());
+        c.add(Gate::unitary(GateMatrix(k, std::move(m)), std::move(t), std::move(ctl), "FUSED"));
+    };
+    auto add_phase = [&](std::vector<int> ctl, Amp e, int anchor) {
+        // phase e on the all-ones pattern of ctl (global phase when ctl is empty)
+        if (ctl.empty()) {
+            add_matrix({anchor}, {}, {e, 0.0, 0.0, e});
+            return;
         }
-        c.add(Gate::unitary(GateMatrix(k, std::move(m)), t, ctl, "FUSED"));
+        const int t = ctl.back();
+        ctl.pop_back();
+        add_matrix({t}, ctl, {1.0, 0.0, 0.0, e});
+    };
+    for (const Op& o : ops) {
+        switch (o.kind) {
+        case OpKind::Fence: break;
+        case OpKind::Dense: add_matrix(o.qubits, o.controls, o.data); break;
+        case OpKind::XPerm: add_matrix(o.qubits, o.controls, {0.0, 1.0, 1.0, 0.0}); break;
+        case OpKind::Diag:
+            if (o.qubits.empty()) {
+                add_phase(o.controls, o.data[0], 0);
+            } else {
+                const std::size_t D = o.data.size();
+                std::vector<Amp> m(D * D, Amp{0.0, 0.0});
+                for (std::size_t i = 0; i < D; ++i)
+                    m[i * D + i] = o.data[i];
+                add_matrix(o.qubits, o.controls, m);
+            }
+            break;
+        case OpKind::PhaseProd:
+            add_phase(o.controls, o.data[0], 0);
+            for (const auto& f : o.factors) {
+                std::vector<int> ctl = o.controls;
+                ctl.push_back(f.first);
+                add_phase(ctl, f.second, 0);
+            }
+            break;
+        case OpKind::RBlock:
+            for (const Prim& p : o.prims) {
+                const std::vector<int>& s = o.qubits;
+                if (p.kind == QSV_PRIM_U1) {
+                    add_matrix({s[p.a]}, {}, p.data);
+                } else if (p.kind == QSV_PRIM_U2) {
+                    add_matrix({s[p.a], s[p.b]}, {}, p.data);
+                } else if (p.kind == QSV_PRIM_CX) {
+                    add_matrix({s[p.b]}, {s[p.a]}, {0.0, 1.0, 1.0, 0.0});
+                } else {
+                    const int nb = static_cast<int>(s.size());
+                    const std::size_t D = std::size_t{1} << nb;
+                    std::vector<Amp> m(D * D, Amp{0.0, 0.0});
+                    for (std::size_t i = 0; i < D; ++i)
+                        m[i * D + i] = p.data[i];
+                    add_matrix(s, {}, m);
+                }
+            }
+            break;
+        }
     }
     return c;
 }

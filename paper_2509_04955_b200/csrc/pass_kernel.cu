@@ -37,7 +37,7 @@ namespace qsv {
 
 namespace {
 
-constexpr int kNumBuf = 3;
+constexpr int kNumBuf = 2;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -121,67 +121,73 @@ __device__ __forceinline__ uint32_t deposit(uint32_t g, const int8_t* fixpos, in
     return g;
 }
 
-// ---------------------------------------------------------------- ops
-template <int KK>
-__device__ __forceinline__ void dense_rows(double2* tile, const double2* M, const uint32_t* off,
-                                           uint32_t b, const double2 (&v)[1 << KK], int r0,
-                                           int nrows) {
-    constexpr int D = 1 << KK;
-    // Two rows per iteration: four independent DFMA chains per thread.
-#pragma unroll 1
-    for (int r = r0; r < r0 + nrows; r += 2) {
-        const double2* row0 = M + r * D;
-        const double2* row1 = row0 + D;
-        double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            cmac(a0, row0[j], v[j]);
-            cmac(a1, row1[j], v[j]);
-        }
-        tile[b | off[r]] = a0;
-        tile[b | off[r + 1]] = a1;
-    }
+// Groups of an op are enumerated directly in "deposited" form: with F the
+// mask of the op's fixed tile bits (targets + tile controls), the successor of
+// b = deposit(g) after a stride s is ((b | F) + deposit(s)) & ~F — the fixed
+// bits, forced to 1, carry the addition across themselves.  Three integer ops
+// per group instead of a loop over the fixed positions.
+__device__ __forceinline__ uint32_t next_group(uint32_t b, uint32_t F, uint32_t dstride) {
+    return ((b | F) + dstride) & ~F;
 }
 
+// ---------------------------------------------------------------- ops
+// Warp-level complex mat-vec for k <= 4 (D = 2^k <= 16).  LPG = D*S lanes
+// cooperate on one 2^k-amplitude group: lane (r, s) keeps columns
+// [s*D/S, (s+1)*D/S) of matrix row r in registers for the whole op, reads the
+// group members as SMEM broadcasts, and the S partial sums of a row are
+// combined with warp shuffles.  A warp processes 32/LPG groups per step, so
+// registers stay ~8*D/S per lane and no CTA barrier is needed inside the op
+// (only __syncwarp between the reads and the in-place writes of a group).
 template <int KK, int K, int NT>
 __device__ __forceinline__ void dense_op(double2* tile, const TileOp& op, const unsigned char* blob) {
     constexpr int D = 1 << KK;
-    const int nfix = op.nfix;
-    const uint32_t tctrl = op.tctrl;
-    const uint32_t groups = 1u << (K - nfix);
+    constexpr int S = D >= 8 ? 2 : 1;     // column splits
+    constexpr int LPG = D * S;            // lanes per group
+    constexpr int GPW = 32 / LPG;         // groups per warp step
+    constexpr int CPL = D / S;            // columns per lane
+    constexpr int NW = NT / 32;
+    constexpr uint32_t PER_STEP = NW * GPW;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int sub = lane / LPG;
+    const int r = (lane % LPG) / S;
+    const int sp = (lane % LPG) % S;
     const double2* M = reinterpret_cast<const double2*>(blob + op.mat_byte);
     const uint32_t* off = reinterpret_cast<const uint32_t*>(blob + op.off_byte);
-    if (groups >= static_cast<uint32_t>(NT)) {
-        // One thread owns whole groups: read all 2^k members, then overwrite them.
+    double2 m[CPL];
+    uint32_t o[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        m[c] = M[r * D + sp * CPL + c];
+        o[c] = off[sp * CPL + c];
+    }
+    const uint32_t my_off = off[r];
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    const uint32_t g = static_cast<uint32_t>(warp * GPW + sub);
+    uint32_t b = deposit(g, op.fixpos, nfix);
+    const uint32_t dstep = deposit(PER_STEP, op.fixpos, nfix);
+    const uint32_t steps = groups >= PER_STEP ? groups / PER_STEP : 1u;
+    const bool act = g < groups;
 #pragma unroll 1
-        for (uint32_t g = threadIdx.x; g < groups; g += NT) {
-            const uint32_t b = deposit(g, op.fixpos, nfix) | tctrl;
-            double2 v[D];
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t idx = b | tctrl;
+        double2 acc = make_double2(0.0, 0.0);
+        if (act) {
 #pragma unroll
-            for (int j = 0; j < D; ++j)
-                v[j] = tile[b | off[j]];
-            dense_rows<KK>(tile, M, off, b, v, 0, D);
+            for (int c = 0; c < CPL; ++c)
+                cmac(acc, m[c], tile[idx | o[c]]);
         }
-    } else {
-        // Fewer groups than threads: R threads share a group, each computing
-        // D/R (>= 2) output rows.  All inputs are read before any output is written.
-        const int R = min(NT / static_cast<int>(groups), D / 2);
-        const int rows = D / R;
-        const int t = threadIdx.x;
-        const bool active = t < static_cast<int>(groups) * R;
-        const uint32_t g = static_cast<uint32_t>(t) % groups;
-        const int rb = t / static_cast<int>(groups);
-        double2 v[D];
-        uint32_t b = 0;
-        if (active) {
-            b = deposit(g, op.fixpos, nfix) | tctrl;
-#pragma unroll
-            for (int j = 0; j < D; ++j)
-                v[j] = tile[b | off[j]];
+        if constexpr (S > 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
         }
-        __syncthreads();
-        if (active)
-            dense_rows<KK>(tile, M, off, b, v, rb * rows, rows);
+        __syncwarp();
+        if (act && sp == 0)
+            tile[idx | my_off] = acc;
+        b = next_group(b, F, dstep);
     }
 }
 
@@ -189,14 +195,22 @@ template <int K, int NT>
 __device__ __forceinline__ void xperm_op(double2* tile, const TileOp& op) {
     const int nfix = op.nfix;
     const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
     const uint32_t groups = 1u << (K - nfix);
     const uint32_t tb = 1u << op.tpos[0];
-    for (uint32_t g = threadIdx.x; g < groups; g += NT) {
-        const uint32_t b = deposit(g, op.fixpos, nfix) | tctrl;
-        const double2 a0 = tile[b];
-        const double2 a1 = tile[b | tb];
-        tile[b] = a1;
-        tile[b | tb] = a0;
+    if (threadIdx.x >= groups)
+        return;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+#pragma unroll 2
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t idx = b | tctrl;
+        const double2 a0 = tile[idx];
+        const double2 a1 = tile[idx | tb];
+        tile[idx] = a1;
+        tile[idx | tb] = a0;
+        b = next_group(b, F, dstep);
     }
 }
 
@@ -205,31 +219,253 @@ __device__ __forceinline__ void diag_op(double2* tile, const TileOp& op, const u
                                         uint64_t full_base) {
     const int nfix = op.nfix;
     const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
     const uint32_t groups = 1u << (K - nfix);
     const int k = op.k;
     const int nin = op.nin;
-    const uint32_t tmask = op.tmask;
     const double2* Dg = reinterpret_cast<const double2*>(blob + op.mat_byte);
     uint32_t e0 = 0;
     for (int j = nin; j < k; ++j)
         e0 |= static_cast<uint32_t>((full_base >> op.xbit[j - nin]) & 1ull) << j;
+    if (threadIdx.x >= groups)
+        return;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
     if (nin == 0) {
         const double2 d = Dg[e0];
-        for (uint32_t g = threadIdx.x; g < groups; g += NT) {
-            const uint32_t idx = deposit(g, op.fixpos, nfix) | tctrl;
+#pragma unroll 4
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t idx = b | tctrl;
             tile[idx] = cmul(d, tile[idx]);
+            b = next_group(b, F, dstep);
         }
-        return;
+    } else if (nin == 1) {
+        const int p = __ffs(op.tmask) - 1;
+        const double2 d0 = Dg[e0], d1 = Dg[e0 | 1u];
+#pragma unroll 4
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t idx = b | tctrl;
+            tile[idx] = cmul(((idx >> p) & 1u) ? d1 : d0, tile[idx]);
+            b = next_group(b, F, dstep);
+        }
+    } else {
+        const uint8_t* plo = blob + op.ptab_byte;
+        const uint8_t* phi = plo + 32;
+#pragma unroll 2
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t idx = b | tctrl;
+            const uint32_t e = e0 | plo[idx & 31u] | phi[idx >> 5];
+            tile[idx] = cmul(Dg[e], tile[idx]);
+            b = next_group(b, F, dstep);
+        }
     }
-    for (uint32_t g = threadIdx.x; g < groups; g += NT) {
-        const uint32_t idx = deposit(g, op.fixpos, nfix) | tctrl;
-        uint32_t e = e0, m = tmask;
-        for (int i = 0; m; ++i) {
-            const int p = __ffs(m) - 1;
-            e |= ((idx >> p) & 1u) << i;
-            m &= m - 1;
+}
+
+// k = 5 (D = 32): one thread per group, all 32 members in registers.
+template <int K, int NT>
+__device__ __forceinline__ void dense5_op(double2* tile, const TileOp& op, const unsigned char* blob) {
+    constexpr int D = 32;
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t groups = 1u << (K - nfix);
+    const double2* M = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    const uint32_t* off = reinterpret_cast<const uint32_t*>(blob + op.off_byte);
+    const bool many = groups >= static_cast<uint32_t>(NT);
+    const int R = many ? 1 : min(NT / static_cast<int>(groups), D);
+    const int rows = D / R;
+#pragma unroll 1
+    for (uint32_t base_t = 0; base_t < (many ? groups : 1u); base_t += NT) {
+        const int t = static_cast<int>(threadIdx.x);
+        const uint32_t g = many ? base_t + t : static_cast<uint32_t>(t) % groups;
+        const int rb = many ? 0 : t / static_cast<int>(groups);
+        const bool act = many ? g < groups : t < static_cast<int>(groups) * R;
+        double2 v[D];
+        uint32_t b = 0;
+        if (act) {
+            b = deposit(g, op.fixpos, nfix) | tctrl;
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                v[j] = tile[b | off[j]];
         }
-        tile[idx] = cmul(Dg[e], tile[idx]);
+        if (!many)
+            __syncthreads();
+        if (act) {
+#pragma unroll 1
+            for (int rr = 0; rr < rows; ++rr) {
+                const int row = rb * rows + rr;
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < D; ++j)
+                    cmac(acc, M[row * D + j], v[j]);
+                tile[b | off[row]] = acc;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- RBLOCK
+// A register block holds one 16-amplitude group (4 block qubits) per thread and
+// applies a list of native gates to it in registers; the list is uniform over
+// the CTA, so the per-primitive switch is a uniform branch.  Amplitude j of the
+// group has block-qubit i in bit i of j.
+template <int Q>
+__device__ __forceinline__ void rb_u1(double2 (&v)[16], const double2* U) {
+    const double2 u00 = U[0], u01 = U[1], u10 = U[2], u11 = U[3];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j & (1 << Q))
+            continue;
+        const double2 x0 = v[j], x1 = v[j | (1 << Q)];
+        double2 r0 = make_double2(0.0, 0.0), r1 = make_double2(0.0, 0.0);
+        cmac(r0, u00, x0);
+        cmac(r0, u01, x1);
+        cmac(r1, u10, x0);
+        cmac(r1, u11, x1);
+        v[j] = r0;
+        v[j | (1 << Q)] = r1;
+    }
+}
+
+template <int A, int B>  // A < B: matrix bit 0 <-> block qubit A, bit 1 <-> B
+__device__ __forceinline__ void rb_u2(double2 (&v)[16], const double2* M) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (j & ((1 << A) | (1 << B)))
+            continue;
+        const int i1 = j | (1 << A), i2 = j | (1 << B), i3 = j | (1 << A) | (1 << B);
+        const double2 x0 = v[j], x1 = v[i1], x2 = v[i2], x3 = v[i3];
+        double2 y[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double2 acc = make_double2(0.0, 0.0);
+            cmac(acc, M[4 * r + 0], x0);
+            cmac(acc, M[4 * r + 1], x1);
+            cmac(acc, M[4 * r + 2], x2);
+            cmac(acc, M[4 * r + 3], x3);
+            y[r] = acc;
+        }
+        v[j] = y[0];
+        v[i1] = y[1];
+        v[i2] = y[2];
+        v[i3] = y[3];
+    }
+}
+
+template <int C, int T>  // X on T controlled by C
+__device__ __forceinline__ void rb_cx(double2 (&v)[16]) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        if (!(j & (1 << C)) || (j & (1 << T)))
+            continue;
+        const double2 t = v[j];
+        v[j] = v[j | (1 << T)];
+        v[j | (1 << T)] = t;
+    }
+}
+
+__device__ __forceinline__ void rb_diag(double2 (&v)[16], const double2* D) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        v[j] = cmul(D[j], v[j]);
+}
+
+#define RB_CODE(kind, a, b) (((kind) << 4) | ((a) << 2) | (b))
+
+__device__ __forceinline__ void rb_apply(double2 (&v)[16], const DevPrim pr, const double2* m) {
+    switch (RB_CODE(pr.kind, pr.a, pr.b)) {
+    case RB_CODE(QSV_PRIM_U1, 0, 0): rb_u1<0>(v, m); break;
+    case RB_CODE(QSV_PRIM_U1, 1, 0): rb_u1<1>(v, m); break;
+    case RB_CODE(QSV_PRIM_U1, 2, 0): rb_u1<2>(v, m); break;
+    case RB_CODE(QSV_PRIM_U1, 3, 0): rb_u1<3>(v, m); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 1): rb_u2<0, 1>(v, m); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 2): rb_u2<0, 2>(v, m); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 3): rb_u2<0, 3>(v, m); break;
+    case RB_CODE(QSV_PRIM_U2, 1, 2): rb_u2<1, 2>(v, m); break;
+    case RB_CODE(QSV_PRIM_U2, 1, 3): rb_u2<1, 3>(v, m); break;
+    case RB_CODE(QSV_PRIM_U2, 2, 3): rb_u2<2, 3>(v, m); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 1): rb_cx<0, 1>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 2): rb_cx<0, 2>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 3): rb_cx<0, 3>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 0): rb_cx<1, 0>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 2): rb_cx<1, 2>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 3): rb_cx<1, 3>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 0): rb_cx<2, 0>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 1): rb_cx<2, 1>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 3): rb_cx<2, 3>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 3, 0): rb_cx<3, 0>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 3, 1): rb_cx<3, 1>(v); break;
+    case RB_CODE(QSV_PRIM_CX, 3, 2): rb_cx<3, 2>(v); break;
+    default: rb_diag(v, m); break;  // QSV_PRIM_DIAG16
+    }
+}
+
+template <int K, int NT>
+__device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const unsigned char* blob) {
+    const uint32_t m0 = 1u << op.tpos[0], m1 = 1u << op.tpos[1];
+    const uint32_t m2 = 1u << op.tpos[2], m3 = 1u << op.tpos[3];
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    if (threadIdx.x >= groups)
+        return;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+    const DevPrim* prims = reinterpret_cast<const DevPrim*>(blob + op.prim_byte);
+    const int np = op.nprim;
+#pragma unroll 1
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t idx = b | tctrl;
+        double2 v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            v[j] = tile[idx | ((j & 1) ? m0 : 0u) | ((j & 2) ? m1 : 0u) | ((j & 4) ? m2 : 0u) |
+                        ((j & 8) ? m3 : 0u)];
+#pragma unroll 1
+        for (int p = 0; p < np; ++p) {
+            const DevPrim pr = prims[p];
+            rb_apply(v, pr, reinterpret_cast<const double2*>(blob + pr.data_byte));
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            tile[idx | ((j & 1) ? m0 : 0u) | ((j & 2) ? m1 : 0u) | ((j & 4) ? m2 : 0u) |
+                 ((j & 8) ? m3 : 0u)] = v[j];
+        b = next_group(b, F, dstep);
+    }
+}
+
+// ---------------------------------------------------------------- PHASEPROD
+// amp *= c * prod_{q in Q, bit q set} f_q for amplitudes with the controls set.
+// In-tile factors are pre-tabulated over the low 5 tile bits (A[32]) and the
+// high tile bits (B[64]); out-of-tile factors collapse into a CTA constant.
+template <int K, int NT>
+__device__ __forceinline__ void phaseprod_op(double2* tile, const TileOp& op, const unsigned char* blob,
+                                             uint64_t full_base) {
+    const double2* tab = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    const ExtFactor* ext = reinterpret_cast<const ExtFactor*>(blob + op.prim_byte);
+    double2 c = tab[0];
+    for (int i = 0; i < op.nprim; ++i)
+        if ((full_base >> ext[i].bit) & 1ull)
+            c = cmul(c, make_double2(ext[i].re, ext[i].im));
+    const double2* A = tab + 1;
+    const double2* B = tab + 33;
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    if (threadIdx.x >= groups)
+        return;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+#pragma unroll 4
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t idx = b | tctrl;
+        const double2 w = cmul(c, cmul(A[idx & 31u], B[idx >> 5]));
+        tile[idx] = cmul(w, tile[idx]);
+        b = next_group(b, F, dstep);
     }
 }
 
@@ -248,8 +484,14 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const GeomArg& g) {
     return base;
 }
 
+// Resident CTAs per SM the register allocation must allow.
+template <int KMAX, int NT>
+constexpr int min_ctas() {
+    return NT < 128 ? 1 : (KMAX <= 4 ? 3 : 1);
+}
+
 template <int K, int KMAX, int NT>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, min_ctas<KMAX, NT>())
 pass_kernel(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, uint32_t blob_bytes,
             int nops, const __grid_constant__ GeomArg geom, uint64_t rank_base, uint64_t ntiles) {
     constexpr int TILE = 1 << K;
@@ -282,15 +524,20 @@ pass_kernel(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, 
     __syncthreads();
 
     const uint64_t stride = gridDim.x;
+    // Warp 0 drives the TMA bulk engine: lane 0 arms the tile's mbarrier with the
+    // byte count, then the 32 lanes issue the 2^nhigh run copies between them.
+    const int lane = threadIdx.x & 31;
     auto issue_load = [&](uint64_t t, int b) {
         const uint64_t base = tile_base(t, geom);
         double2* dst = bufs + b * TILE;
-        mbar_expect_tx(&mbar[b], static_cast<uint32_t>(sizeof(double2) * TILE));
-        for (int j = 0; j < nh; ++j)
+        if (lane == 0)
+            mbar_expect_tx(&mbar[b], static_cast<uint32_t>(sizeof(double2) * TILE));
+        __syncwarp();
+        for (int j = lane; j < nh; j += 32)
             bulk_load(dst + (j << L), psi + base + hi_off[j], run_bytes, &mbar[b]);
     };
 
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         for (int s = 0; s < kNumBuf - 1; ++s) {
             const uint64_t t = blockIdx.x + s * stride;
             if (t < ntiles)
@@ -302,11 +549,13 @@ pass_kernel(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, 
     int it = 0;
     for (uint64_t t = blockIdx.x; t < ntiles; t += stride, ++it) {
         const int b = it % kNumBuf;
-        if (threadIdx.x == 0) {
+        if (threadIdx.x < 32) {
             const uint64_t tn = t + (kNumBuf - 1) * stride;
             if (tn < ntiles) {
-                // Buffer (it + NBUF - 1) % NBUF was last stored from in iteration it - 1.
+                // Buffer (it + NBUF - 1) % NBUF was last stored from in iteration
+                // it - 1: every lane waits for its own store groups to finish reading.
                 bulk_wait_read_all();
+                __syncwarp();
                 issue_load(tn, (it + kNumBuf - 1) % kNumBuf);
             }
         }
@@ -326,7 +575,11 @@ pass_kernel(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, 
                 if constexpr (KMAX >= 2 && K >= 2) { if (kk == 2) dense_op<2, K, NT>(tile, op, blob); }
                 if constexpr (KMAX >= 3 && K >= 3) { if (kk == 3) dense_op<3, K, NT>(tile, op, blob); }
                 if constexpr (KMAX >= 4 && K >= 4) { if (kk == 4) dense_op<4, K, NT>(tile, op, blob); }
-                if constexpr (KMAX >= 5 && K >= 5) { if (kk == 5) dense_op<5, K, NT>(tile, op, blob); }
+                if constexpr (KMAX >= 5 && K >= 5) { if (kk == 5) dense5_op<K, NT>(tile, op, blob); }
+            } else if (op.kind == QSV_OP_RBLOCK) {
+                if constexpr (K >= 4) rblock_op<K, NT>(tile, op, blob);
+            } else if (op.kind == QSV_OP_PHASEPROD) {
+                phaseprod_op<K, NT>(tile, op, blob, full_base);
             } else if (op.kind == QSV_OP_DIAG) {
                 diag_op<K, NT>(tile, op, blob, full_base);
             } else {
@@ -337,19 +590,19 @@ pass_kernel(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, 
         // (async) proxy, then let thread 0 stream the tile back.
         fence_proxy_async();
         __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int j = 0; j < nh; ++j)
+        if (threadIdx.x < 32) {
+            for (int j = lane; j < nh; j += 32)
                 bulk_store(psi + base + hi_off[j], tile + (j << L), run_bytes);
             bulk_commit();
         }
     }
-    if (threadIdx.x == 0)
+    if (threadIdx.x < 32)
         bulk_wait_all();
 }
 
 template <int K>
 constexpr int threads_for() {
-    return K >= 8 ? 256 : (K >= 6 ? 64 : 32);
+    return K >= 8 ? 128 : (K >= 6 ? 64 : 32);
 }
 
 template <int K, int KMAX>

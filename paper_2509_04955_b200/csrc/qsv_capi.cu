@@ -411,8 +411,9 @@ struct BlobBuilder {
 };
 
 int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
-                 const qsv_op_desc* ops, int nops, const double* pool, size_t pool_len,
-                 qsv::Step& step, std::vector<unsigned char>& blob_out) {
+                 const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims, int nprims,
+                 const double* pool, size_t pool_len, qsv::Step& step,
+                 std::vector<unsigned char>& blob_out) {
     using qsv::TileOp;
     const int K = d.tile_k;
     QSV_REQUIRE(K >= 1 && K <= 11 && K <= n_local, "pass: tile_k must be in [1, min(11, n_local)]");
@@ -440,7 +441,8 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
     const uint64_t full_mask = (n_total >= 64) ? ~0ull : ((1ull << n_total) - 1ull);
     const uint64_t rank_bits = static_cast<uint64_t>(rank) << n_local;
     std::vector<TileOp> tops(d.op_count);
-    struct Payload { int op; std::vector<uint32_t> off; std::vector<double> data; };
+    struct Payload { int op; std::vector<uint32_t> off; std::vector<double> data; std::vector<uint8_t> ptab;
+                     std::vector<qsv::DevPrim> dprims; std::vector<std::vector<double>> pdata; std::vector<qsv::ExtFactor> ext; };
     std::vector<Payload> payloads;
     double flops = 0.0;
     const double amps = std::ldexp(1.0, n_local);
@@ -505,6 +507,108 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                 step.geom.kmax = std::max(step.geom.kmax, od.k);
                 flops += 8.0 * D * amps * frac;
             }
+        } else if (od.kind == QSV_OP_RBLOCK) {
+            QSV_REQUIRE(od.k == 4, "op: RBLOCK needs exactly 4 block qubits");
+            QSV_REQUIRE(od.prim_begin >= 0 && od.nprim >= 1 && od.prim_begin + od.nprim <= nprims,
+                        "op: RBLOCK primitive range outside the primitive array");
+            QSV_REQUIRE(K >= 4, "op: RBLOCK needs a tile of >= 4 qubits");
+            for (int i = 0; i < 4; ++i) {
+                const int q = od.qubits[i];
+                QSV_REQUIRE(q < n_local && tpos_of[q] >= 0,
+                            "op: RBLOCK qubit " + std::to_string(q) + " is not in the pass tile");
+                t.tpos[i] = static_cast<int8_t>(tpos_of[q]);
+                fix.push_back(tpos_of[q]);
+            }
+            for (int pi = 0; pi < od.nprim; ++pi) {
+                const qsv_prim_desc& pd = prims[od.prim_begin + pi];
+                qsv::DevPrim dp{};
+                dp.kind = static_cast<uint8_t>(pd.kind);
+                dp.a = static_cast<uint8_t>(pd.a);
+                dp.b = static_cast<uint8_t>(pd.b);
+                int ne = 0;
+                double fl = 0;
+                switch (pd.kind) {
+                case QSV_PRIM_U1:
+                    QSV_REQUIRE(pd.a >= 0 && pd.a < 4, "prim: U1 qubit index outside 0..3");
+                    dp.b = 0;
+                    ne = 4;
+                    fl = 16;
+                    break;
+                case QSV_PRIM_U2:
+                    QSV_REQUIRE(pd.a >= 0 && pd.b > pd.a && pd.b < 4, "prim: U2 needs 0 <= a < b < 4");
+                    ne = 16;
+                    fl = 32;
+                    break;
+                case QSV_PRIM_CX:
+                    QSV_REQUIRE(pd.a >= 0 && pd.a < 4 && pd.b >= 0 && pd.b < 4 && pd.a != pd.b,
+                                "prim: CX needs distinct block qubits");
+                    break;
+                case QSV_PRIM_DIAG16:
+                    dp.a = 3;  // routes to the default (diagonal) case of the switch
+                    dp.b = 3;
+                    ne = 16;
+                    fl = 6;
+                    break;
+                default:
+                    QSV_REQUIRE(false, "prim: unknown RBLOCK primitive kind");
+                }
+                if (ne) {
+                    QSV_REQUIRE(pd.mat_off >= 0 && static_cast<size_t>(pd.mat_off) + ne <= pool_len,
+                                "prim: matrix outside the pool");
+                    pl.pdata.emplace_back(pool + 2 * pd.mat_off, pool + 2 * (pd.mat_off + ne));
+                } else {
+                    pl.pdata.emplace_back();
+                }
+                pl.dprims.push_back(dp);
+                flops += fl * amps * frac;
+            }
+            t.nprim = od.nprim;
+            step.geom.kmax = std::max(step.geom.kmax, 1);
+        } else if (od.kind == QSV_OP_PHASEPROD) {
+            QSV_REQUIRE(od.k == 0, "op: PHASEPROD takes its qubits as FACTOR primitives (k = 0)");
+            QSV_REQUIRE(od.prim_begin >= 0 && od.nprim >= 0 && od.prim_begin + od.nprim <= nprims,
+                        "op: PHASEPROD primitive range outside the primitive array");
+            QSV_REQUIRE(od.mat_off >= 0 && static_cast<size_t>(od.mat_off) + 1 <= pool_len,
+                        "op: PHASEPROD constant outside the pool");
+            // table: [c][A: 32 low tile bits][B: 64 high tile bits]
+            std::vector<double> tab(2 * 97, 0.0);
+            for (int e = 0; e < 97; ++e)
+                tab[2 * e] = 1.0;
+            tab[0] = pool[2 * od.mat_off];
+            tab[1] = pool[2 * od.mat_off + 1];
+            auto mul_into = [&](int e, double fr, double fi) {
+                const double r = tab[2 * e], im = tab[2 * e + 1];
+                tab[2 * e] = r * fr - im * fi;
+                tab[2 * e + 1] = r * fi + im * fr;
+            };
+            for (int pi = 0; pi < od.nprim; ++pi) {
+                const qsv_prim_desc& pd = prims[od.prim_begin + pi];
+                QSV_REQUIRE(pd.kind == QSV_PRIM_FACTOR, "prim: PHASEPROD accepts FACTOR primitives only");
+                QSV_REQUIRE(pd.a >= 0 && pd.a < n_total, "prim: FACTOR qubit out of range");
+                QSV_REQUIRE(pd.mat_off >= 0 && static_cast<size_t>(pd.mat_off) + 1 <= pool_len,
+                            "prim: FACTOR value outside the pool");
+                const double fr = pool[2 * pd.mat_off], fi = pool[2 * pd.mat_off + 1];
+                const int q = pd.a;
+                const int tp = (q < n_local) ? tpos_of[q] : -1;
+                if (tp >= 0 && tp < 5) {
+                    for (int e = 0; e < 32; ++e)
+                        if (e >> tp & 1)
+                            mul_into(1 + e, fr, fi);
+                } else if (tp >= 5) {
+                    for (int e = 0; e < 64; ++e)
+                        if (e >> (tp - 5) & 1)
+                            mul_into(33 + e, fr, fi);
+                } else {
+                    qsv::ExtFactor xf{};
+                    xf.re = fr;
+                    xf.im = fi;
+                    xf.bit = q;
+                    pl.ext.push_back(xf);
+                }
+            }
+            pl.data = std::move(tab);
+            t.nprim = static_cast<int32_t>(pl.ext.size());
+            flops += 18.0 * amps * frac;
         } else if (od.kind == QSV_OP_DIAG) {
             QSV_REQUIRE(od.k >= 0 && od.k <= QSV_MAX_DIAG_K, "op: diagonal arity must be in [0, 8]");
             const int D = 1 << od.k;
@@ -547,10 +651,26 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
         std::sort(fix.begin(), fix.end());
         QSV_REQUIRE(fix.size() <= sizeof(t.fixpos), "op: too many fixed tile bits");
         t.nfix = static_cast<int32_t>(fix.size());
-        for (size_t i = 0; i < fix.size(); ++i)
+        for (size_t i = 0; i < fix.size(); ++i) {
             t.fixpos[i] = static_cast<int8_t>(fix[i]);
+            t.fmask |= 1u << fix[i];
+        }
+        if (od.kind == QSV_OP_DIAG && t.nin > 0) {
+            // pext(idx, tmask) = ptab_lo[idx & 31] | ptab_hi[idx >> 5]  (K <= 11)
+            pl.ptab.resize(96);
+            for (int j = 0; j < 96; ++j) {
+                const uint32_t idx = j < 32 ? static_cast<uint32_t>(j) : static_cast<uint32_t>(j - 32) << 5;
+                uint32_t e = 0, m = t.tmask;
+                for (int bit = 0; m; ++bit) {
+                    const int pbit = __builtin_ctz(m);
+                    e |= ((idx >> pbit) & 1u) << bit;
+                    m &= m - 1;
+                }
+                pl.ptab[j] = static_cast<uint8_t>(e);
+            }
+        }
         tops[oi] = t;
-        if (!pl.data.empty() || !pl.off.empty())
+        if (!pl.data.empty() || !pl.off.empty() || !pl.ptab.empty() || !pl.dprims.empty() || !pl.ext.empty())
             payloads.push_back(std::move(pl));
     }
     BlobBuilder bb;
@@ -561,6 +681,16 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
             t.off_byte = bb.append(pl.off.data(), pl.off.size() * sizeof(uint32_t));
         if (!pl.data.empty())
             t.mat_byte = bb.append(pl.data.data(), pl.data.size() * sizeof(double));
+        if (!pl.ptab.empty())
+            t.ptab_byte = bb.append(pl.ptab.data(), pl.ptab.size());
+        if (!pl.dprims.empty()) {
+            for (size_t i = 0; i < pl.dprims.size(); ++i)
+                if (!pl.pdata[i].empty())
+                    pl.dprims[i].data_byte = bb.append(pl.pdata[i].data(), pl.pdata[i].size() * sizeof(double));
+            t.prim_byte = bb.append(pl.dprims.data(), pl.dprims.size() * sizeof(qsv::DevPrim));
+        }
+        if (!pl.ext.empty())
+            t.prim_byte = bb.append(pl.ext.data(), pl.ext.size() * sizeof(qsv::ExtFactor));
     }
     std::memcpy(bb.bytes.data(), tops.data(), tops.size() * sizeof(TileOp));
     bb.bytes.resize((bb.bytes.size() + 15) & ~size_t{15});
@@ -577,8 +707,8 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
 } // namespace
 
 extern "C" int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local, const qsv_step_desc* steps,
-                                  int nsteps, const qsv_op_desc* ops, int nops, const double* pool,
-                                  size_t pool_len, qsv_program** out) {
+                                  int nsteps, const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims,
+                                  int nprims, const double* pool, size_t pool_len, qsv_program** out) {
     QSV_REQUIRE(ctx != nullptr && out != nullptr, "qsv_program_create: null argument");
     QSV_REQUIRE(nsteps >= 0 && (steps != nullptr || nsteps == 0), "qsv_program_create: bad steps");
     QSV_REQUIRE(nops >= 0 && (ops != nullptr || nops == 0), "qsv_program_create: bad ops");
@@ -597,7 +727,8 @@ extern "C" int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local, const 
         s.desc = steps[i];
         if (steps[i].kind == QSV_STEP_PASS) {
             std::vector<unsigned char> blob;
-            int rc = compile_pass(steps[i], n_total, n_local, ctx->rank, ops, nops, pool, pool_len, s, blob);
+            int rc = compile_pass(steps[i], n_total, n_local, ctx->rank, ops, nops, prims, nprims, pool,
+                                  pool_len, s, blob);
             if (rc != QSV_OK) {
                 set_error("step " + std::to_string(i) + ": " + qsv_last_error());
                 delete prog;
@@ -645,8 +776,8 @@ extern "C" int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local, const 
 }
 
 extern "C" int qsv_program_validate(int n_total, int n_local, int rank, const qsv_step_desc* steps,
-                                    int nsteps, const qsv_op_desc* ops, int nops, const double* pool,
-                                    size_t pool_len) {
+                                    int nsteps, const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims,
+                                    int nprims, const double* pool, size_t pool_len) {
     QSV_REQUIRE(nsteps >= 0 && (steps != nullptr || nsteps == 0), "qsv_program_validate: bad steps");
     QSV_REQUIRE(nops >= 0 && (ops != nullptr || nops == 0), "qsv_program_validate: bad ops");
     QSV_REQUIRE(n_total >= 1 && n_total <= QSV_MAX_QUBITS && n_local >= 1 && n_local <= n_total,
@@ -657,7 +788,8 @@ extern "C" int qsv_program_validate(int n_total, int n_local, int rank, const qs
         if (steps[i].kind == QSV_STEP_PASS) {
             qsv::Step s;
             std::vector<unsigned char> blob;
-            const int rc = compile_pass(steps[i], n_total, n_local, rank, ops, nops, pool, pool_len, s, blob);
+            const int rc = compile_pass(steps[i], n_total, n_local, rank, ops, nops, prims, nprims, pool,
+                                        pool_len, s, blob);
             if (rc != QSV_OK) {
                 set_error("step " + std::to_string(i) + ": " + qsv_last_error());
                 return rc;
@@ -839,7 +971,7 @@ extern "C" int qsv_apply_fused(qsv_state* st, int k, const int* targets, uint64_
     sd.op_begin = 0;
     sd.op_count = 1;
     qsv_program* prog = nullptr;
-    int rc = qsv_program_create(ctx, n_total, n_local, &sd, 1, &op, 1, mat,
+    int rc = qsv_program_create(ctx, n_total, n_local, &sd, 1, &op, 1, nullptr, 0, mat,
                                 static_cast<size_t>(1) << (2 * k), &prog);
     if (rc != QSV_OK)
         return rc;

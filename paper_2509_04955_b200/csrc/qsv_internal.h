@@ -30,6 +30,25 @@ struct TileOp {
     int8_t tpos[QSV_MAX_DIAG_K];  // DENSE/XPERM: tile-local position of target i
     int8_t xbit[QSV_MAX_DIAG_K];  // DIAG: full-index bit of out-of-tile qubit j (table bit nin+j)
     int8_t fixpos[24];            // ascending tile positions fixed during group enumeration
+    uint32_t fmask;               // OR of 1 << fixpos[i]
+    uint32_t ptab_byte;           // DIAG: byte offset of pext tables (uint8 [32] low, [64] high)
+    uint32_t prim_byte;           // RBLOCK: DevPrim list; PHASEPROD: ExtFactor list
+    int32_t nprim;
+};
+
+// RBLOCK primitive as stored in the blob.
+struct DevPrim {
+    uint8_t kind;       // QSV_PRIM_U1 / U2 / CX / DIAG16
+    uint8_t a, b;       // block-local qubit indices (0..3)
+    uint8_t pad;
+    uint32_t data_byte; // blob offset of the matrix / table
+};
+
+// PHASEPROD factor on a qubit outside the tile (CTA-uniform).
+struct ExtFactor {
+    double re, im;
+    int32_t bit;        // full-index bit
+    int32_t pad[3];
 };
 static_assert(sizeof(TileOp) % 16 == 0, "TileOp must keep 16-B alignment in the blob");
 
