@@ -89,7 +89,7 @@ int qsim_engine_upload(qsim_engine* e, const double* amps, uint64_t offset, uint
 int qsim_engine_download(qsim_engine* e, double* amps, uint64_t offset, uint64_t count);
 int qsim_engine_run(qsim_engine* e);           /* enqueue (asynchronous) */
 int qsim_engine_sync(qsim_engine* e);
-int qsim_engine_time(qsim_engine* e, int iters, float* ms);
+int qsim_engine_time(qsim_engine* e, int iters, int64_t basis, float* ms);
 int qsim_engine_norm_sq(qsim_engine* e, double* out);
 int qsim_engine_max_abs_diff(qsim_engine* e, const double* ref, uint64_t offset, uint64_t count,
                              double* out);
@@ -99,6 +99,12 @@ int qsim_engine_nsteps(qsim_engine* e);
 int qsim_engine_step_info(qsim_engine* e, int i, int* kind, int* nops, double* hbm_bytes, double* flops,
                           double* nvl_bytes);
 int qsim_engine_profile(qsim_engine* e, float* ms_per_step);
+
+/* ---- memtrack (ref memtrack.hpp:12-26) scripted session, for parity tests ----
+ * ops[2*i] = kind (0 enable, 1 register_thread, 2 set_phase, 3 on_alloc,
+ * 4 on_free, 5 reset, 6 disable), ops[2*i+1] = argument; writes
+ * peak_bytes(rank, phase) for rank < nranks, phase < 2. */
+void qsim_memtrack_script(const long long* ops, int nops, int nranks, unsigned long long* peaks);
 
 /* ---- reference-facing single call: run_local on host amplitudes ---------
  * Uploads `amps` (2^n interleaved complex, ideally pinned), runs the planned

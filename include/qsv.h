@@ -185,8 +185,10 @@ int qsv_program_run(qsv_state* st, qsv_program* prog);
  * receives per-step device times (profiling aid, not used on the timed path). */
 int qsv_program_profile(qsv_state* st, qsv_program* prog, float* ms_out);
 /* Times `iters` back-to-back runs of the program with CUDA events recorded on
- * the context stream (synchronous); *ms receives the total device time. */
-int qsv_program_time(qsv_state* st, qsv_program* prog, int iters, float* ms);
+ * the context stream (synchronous); *ms receives the total device time.  When
+ * basis >= 0 every run starts with qsv_state_set_basis(basis) inside the
+ * timed region (a full simulation step from a basis state). */
+int qsv_program_time(qsv_state* st, qsv_program* prog, int iters, int64_t basis, float* ms);
 /* Static description of step `i`: algorithmic bytes moved through HBM and
  * DP flops it performs per launch (the roofline numerators). */
 int qsv_program_step_cost(qsv_program* prog, int i, double* hbm_bytes, double* flops,

@@ -285,9 +285,10 @@ class Engine:
     def sync(self):
         _check(load_qsim().qsim_engine_sync(self._h), "sync")
 
-    def time(self, iters: int) -> float:
+    def time(self, iters: int, basis: int = -1) -> float:
+        """Device ms for `iters` runs (each preceded by a reset to |basis> when basis >= 0)."""
         ms = C.c_float()
-        _check(load_qsim().qsim_engine_time(self._h, iters, C.byref(ms)), "time")
+        _check(load_qsim().qsim_engine_time(self._h, iters, C.c_int64(basis), C.byref(ms)), "time")
         return ms.value
 
     def norm_sq(self) -> float:

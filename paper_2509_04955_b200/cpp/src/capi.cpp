@@ -325,10 +325,10 @@ int qsim_engine_sync(qsim_engine* e) {
     });
 }
 
-int qsim_engine_time(qsim_engine* e, int iters, float* ms) {
+int qsim_engine_time(qsim_engine* e, int iters, int64_t basis, float* ms) {
     return guard([&] {
         REQUIRE(e && ms, "qsim_engine_time: null argument");
-        qsim::qsv_check(qsv_program_time(e->st->get(), e->eng->program(), iters, ms), "qsv_program_time");
+        qsim::qsv_check(qsv_program_time(e->st->get(), e->eng->program(), iters, basis, ms), "qsv_program_time");
         return QSV_OK;
     });
 }
@@ -386,6 +386,27 @@ int qsim_engine_profile(qsim_engine* e, float* ms) {
         qsim::qsv_check(qsv_program_profile(e->st->get(), e->eng->program(), ms), "qsv_program_profile");
         return QSV_OK;
     });
+}
+
+void qsim_memtrack_script(const long long* ops, int nops, int nranks, unsigned long long* peaks) {
+    using namespace qsim::memtrack;
+    for (int i = 0; i < nops; ++i) {
+        const long long k = ops[2 * i], a = ops[2 * i + 1];
+        switch (k) {
+        case 0: enable(static_cast<int>(a)); break;
+        case 1: register_thread(static_cast<int>(a)); break;
+        case 2: set_phase(static_cast<Phase>(a)); break;
+        case 3: on_alloc(static_cast<std::size_t>(a)); break;
+        case 4: on_free(static_cast<std::size_t>(a)); break;
+        case 5: reset(); break;
+        case 6: disable(); break;
+        default: break;
+        }
+    }
+    for (int r = 0; r < nranks; ++r)
+        for (int p = 0; p < 2; ++p)
+            peaks[2 * r + p] = peak_bytes(r, static_cast<Phase>(p));
+    unregister_thread();
 }
 
 int qsim_run_local_host(const qsim_circuit* c, const qsim_plan_opts* opts, double* amps) {

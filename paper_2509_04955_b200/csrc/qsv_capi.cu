@@ -807,7 +807,7 @@ extern "C" int qsv_program_validate(int n_total, int n_local, int rank, const qs
     return QSV_OK;
 }
 
-extern "C" int qsv_program_time(qsv_state* st, qsv_program* prog, int iters, float* ms) {
+extern "C" int qsv_program_time(qsv_state* st, qsv_program* prog, int iters, int64_t basis, float* ms) {
     QSV_REQUIRE(st != nullptr && prog != nullptr && ms != nullptr && iters >= 1, "qsv_program_time: bad argument");
     qsv_ctx* ctx = st->ctx;
     QSV_CUDA(cudaSetDevice(ctx->device));
@@ -816,8 +816,12 @@ extern "C" int qsv_program_time(qsv_state* st, qsv_program* prog, int iters, flo
     QSV_CUDA(cudaEventCreate(&b));
     QSV_CUDA(cudaEventRecord(a, ctx->stream));
     int rc = QSV_OK;
-    for (int i = 0; i < iters && rc == QSV_OK; ++i)
-        rc = qsv_program_run(st, prog);
+    for (int i = 0; i < iters && rc == QSV_OK; ++i) {
+        if (basis >= 0)
+            rc = qsv_state_set_basis(st, static_cast<uint64_t>(basis));
+        if (rc == QSV_OK)
+            rc = qsv_program_run(st, prog);
+    }
     QSV_CUDA(cudaEventRecord(b, ctx->stream));
     QSV_CUDA(cudaEventSynchronize(b));
     QSV_CUDA(cudaEventElapsedTime(ms, a, b));

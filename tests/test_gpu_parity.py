@@ -1,0 +1,197 @@
+"""GPU parity: the sm_100a path (libqsv.so through libqsim.so / the C-ABI) against
+the CPU oracle on the same seeded inputs — max-abs <= 1e-10, norm conserved to
+1e-12 (north star), bitwise run-to-run determinism, and the analytic QFT of
+basis states where the CPU cannot hold the state."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+import paper_2509_04955_b200 as pkg
+from oracle import pyoracle as O
+from tests.helpers import (qft_basis_expected, rand_state, rand_unitary, random_mnemonic_circuit,
+                           random_unitary_circuit)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+NORM_TOL = 1e-12
+
+
+def run_gpu(c, a=None, opts=None, basis=None):
+    e = pkg.Engine(c, opts or pkg.PlanOptions())
+    if a is not None:
+        e.upload(a)
+    else:
+        e.set_basis(basis or 0)
+    e.run()
+    e.sync()
+    out = e.download()
+    norm = e.norm_sq()
+    e.close()
+    return out, norm
+
+
+OPTS = {
+    "default": pkg.PlanOptions(),
+    "no-rblock": pkg.PlanOptions(register_blocks=False),
+    "dense4": pkg.PlanOptions(register_blocks=False, fuse_k=4, tile_k=10),
+    "dense5": pkg.PlanOptions(register_blocks=False, fuse_k=5, pass_budget=500),
+    "unfused": pkg.PlanOptions(fusion=False, multi_op_passes=False),
+    "tile8": pkg.PlanOptions(tile_k=8, pass_budget=200),
+}
+
+
+@pytest.mark.parametrize("opt", list(OPTS))
+@pytest.mark.parametrize("spec", ["qft:12", "random:14:10:2", "hea:13:3:4", "uccsd:12:400:3", "qaoa:11:2:1"])
+def test_generated_circuits_vs_oracle(spec, opt):
+    c = pkg.Circuit.generate(spec)
+    a = rand_state(c.n, 1)
+    got, norm = run_gpu(c, a, OPTS[opt])
+    assert np.abs(got - O.run_local(c, a)).max() <= TOL
+    assert abs(norm - 1.0) <= NORM_TOL
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_mnemonic_circuits(seed):  # acceptance #1 on the GPU
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(2, 13))
+    c = random_mnemonic_circuit(n, 50, seed)
+    a = rand_state(n, seed)
+    got, _ = run_gpu(c, a)
+    assert np.abs(got - O.dense_oracle(c, a) if n <= 10 else got - O.run_local(c, a)).max() <= TOL
+
+
+@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("kmax", [2, 4, 5])
+def test_random_dense_unitaries_with_controls(seed, kmax):
+    c = random_unitary_circuit(14, 25, seed, kmax=kmax)
+    a = rand_state(14, seed)
+    for o in (pkg.PlanOptions(fuse_k=min(kmax, 5), pass_budget=400, register_blocks=False), pkg.PlanOptions()):
+        got, norm = run_gpu(c, a, o)
+        assert np.abs(got - O.run_local(c, a)).max() <= TOL
+        assert abs(norm - 1) <= NORM_TOL
+
+
+@pytest.mark.parametrize("t", [0, 1, 4, 5, 9, 10, 15, 19])
+@pytest.mark.parametrize("ctrl", [None, 0, 7, 19])
+def test_single_gate_every_position(t, ctrl):  # Alg. 1/3/4 equivalents, low and high targets
+    if ctrl == t:
+        pytest.skip("control == target")
+    rng = np.random.default_rng(t * 31 + (ctrl or 0))
+    u = rand_unitary(1, rng)
+    c = pkg.Circuit.empty(20).add_unitary(u, [t], [] if ctrl is None else [ctrl])
+    a = rand_state(20, t)
+    got, _ = run_gpu(c, a, pkg.PlanOptions(fusion=False))
+    ref = O.apply_single(a, t, u, "grouped", 8) if ctrl is None else O.apply_controlled(a, ctrl, t, u, 8)
+    assert np.abs(got - ref).max() <= TOL
+
+
+def test_apply_fused_c_abi_direct():  # qsv_apply_fused (SPEC apply_multi) through the raw C-ABI
+    L = pkg.load_qsv()
+    ctx, st = C.c_void_p(), C.c_void_p()
+    assert L.qsv_ctx_create(0, 0, 1, None, C.byref(ctx)) == 0
+    nbytes = C.c_size_t()
+    assert L.qsv_state_alloc(ctx, 16, C.byref(st), C.byref(nbytes)) == 0
+    a = rand_state(16, 5)
+    buf = np.ascontiguousarray(a).view(np.float64)
+    assert L.qsv_state_upload(st, buf.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint64(0), C.c_uint64(1 << 16)) == 0
+    rng = np.random.default_rng(3)
+    ref = a.copy()
+    for targets, ctrls in (([3, 12], [0]), ([15, 1, 7], []), ([2, 9, 11, 14], [5]), ([0, 4, 8, 10, 13], [])):
+        m = rand_unitary(len(targets), rng)
+        mm = np.ascontiguousarray(m).view(np.float64)
+        tg = (C.c_int * len(targets))(*targets)
+        mask = sum(1 << q for q in ctrls)
+        assert L.qsv_apply_fused(st, len(targets), tg, C.c_uint64(mask), mm.ctypes.data_as(C.POINTER(C.c_double))) == 0
+        ref = O.apply_multi(ref, targets, m, ctrls, 8)
+    out = np.empty(1 << 16, dtype=np.complex128)
+    assert L.qsv_state_download(st, out.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), C.c_uint64(0),
+                                C.c_uint64(1 << 16)) == 0
+    assert np.abs(out - ref).max() <= TOL
+    # parameter errors come back as QSV_E_ARG, not a crash
+    tg = (C.c_int * 1)(16)
+    mm = np.eye(2, dtype=np.complex128).view(np.float64)
+    assert L.qsv_apply_fused(st, 1, tg, C.c_uint64(0), mm.ctypes.data_as(C.POINTER(C.c_double))) == -1
+    L.qsv_state_free(st)
+    L.qsv_ctx_destroy(ctx)
+
+
+@pytest.mark.parametrize("x", [0, 0xA5A5A5, 0x123456, (1 << 24) - 1])
+def test_qft24_basis_states_analytic(x):  # BASELINE configs[0], strong analytic form
+    c = pkg.Circuit.generate("qft:24")
+    e = pkg.Engine(c)
+    e.set_basis(x)
+    e.run()
+    assert e.check_qft(x) <= TOL
+    assert abs(e.norm_sq() - 1) <= NORM_TOL
+    if x == 0xA5A5A5:
+        got = e.download()
+        assert np.abs(got - qft_basis_expected(24, x)).max() <= TOL
+    e.close()
+
+
+def test_qft24_random_state_vs_oracle():  # BASELINE configs[0]: same circuit, CPU reference
+    c = pkg.Circuit.generate("qft:24")
+    a = rand_state(24, 1)
+    got, norm = run_gpu(c, a)
+    assert np.abs(got - O.run_local(c, a)).max() <= TOL
+    assert abs(norm - 1) <= NORM_TOL
+
+
+@pytest.mark.parametrize("spec", ["random:22:20:2", "hea:22:5:4", "uccsd:20:3000:3"])
+def test_config_shapes_at_reduced_size(spec):  # configs[1..3] shapes, oracle-checkable sizes
+    c = pkg.Circuit.generate(spec)
+    ref = O.run_local(c)
+    for o in (pkg.PlanOptions(), pkg.PlanOptions(fusion=False)):
+        got, norm = run_gpu(c, None, o)
+        assert np.abs(got - ref).max() <= TOL
+        assert abs(norm - 1) <= NORM_TOL
+
+
+def test_bitwise_determinism_and_digest():
+    c = pkg.Circuit.generate("random:20:10:2")
+    e = pkg.Engine(c)
+    digests = []
+    for _ in range(3):
+        e.set_basis(0)
+        e.run()
+        digests.append(e.digest())
+    assert len(set(digests)) == 1
+    e.close()
+
+
+def test_run_local_host_reference_facing_call():
+    c = pkg.Circuit.generate("hea:16:3:9")
+    a = rand_state(16, 2)
+    got = pkg.run_local_host(c, a)
+    assert np.abs(got - O.run_local(c, a)).max() <= TOL
+
+
+@pytest.mark.parametrize("n", [30])
+def test_large_state_qft_analytic_and_norm(n):  # full-size, checked on the device
+    c = pkg.Circuit.generate(f"qft:{n}")
+    e = pkg.Engine(c)
+    x = 0x2A5A5A5A & ((1 << n) - 1)
+    e.set_basis(x)
+    e.run()
+    assert e.check_qft(x) <= TOL
+    assert abs(e.norm_sq() - 1) <= NORM_TOL
+    e.close()
+
+
+def test_random30_fusion_on_vs_off_and_norm():  # configs[1] at full size: DAGC on vs off
+    c = pkg.Circuit.generate("random:30:20:2")
+    e1 = pkg.Engine(c, pkg.PlanOptions())
+    e1.set_basis(0)
+    e1.run()
+    assert abs(e1.norm_sq() - 1) <= NORM_TOL
+    ref = e1.download(0, 1 << 20)
+    tail = e1.download((1 << 30) - (1 << 20), 1 << 20)
+    e1.close()
+    e2 = pkg.Engine(c, pkg.PlanOptions(fusion=False))
+    e2.set_basis(0)
+    e2.run()
+    assert e2.max_abs_diff(ref, 0) <= TOL
+    assert e2.max_abs_diff(tail, (1 << 30) - (1 << 20)) <= TOL
+    e2.close()
