@@ -90,8 +90,9 @@ struct Plan {
 // Classification helpers.
 std::vector<Op> lower(const Circuit& c);
 std::vector<Op> fuse_ops(const std::vector<Op>& ops, const PlanOptions& opt);
-// Groups ops acting on <= 4 qubits into register blocks (RBLOCK).
-std::vector<Op> form_blocks(const std::vector<Op>& ops);
+// Groups ops acting on <= 4 qubits into register blocks (RBLOCK); a block holds
+// at most max_high qubits at or above min_low (it must fit one pass tile).
+std::vector<Op> form_blocks(const std::vector<Op>& ops, int min_low = 5, int max_high = 6);
 // Relative DP cost per amplitude of one op (the packing / fusion currency).
 double op_cost(const Op& op);
 // Builds the full plan (lower -> fuse -> partition/swaps -> pack).

@@ -217,7 +217,7 @@ int qsim_circuit_fused(const qsim_circuit* c, const qsim_plan_opts* opts, qsim_c
         if (o.fusion) {
             ops = qsim::fuse_ops(ops, o);
             if (o.register_blocks)
-                ops = qsim::form_blocks(ops);
+                ops = qsim::form_blocks(ops, o.min_low, std::max(o.tile_k - o.min_low, 0));
         }
         std::vector<qsim::Op> kept;
         for (auto& op : ops)

@@ -213,7 +213,7 @@ Op make_phaseprod(const Op& A, const Op& B, const std::vector<int>& C, const Fac
 }
 
 // Merge B (later) into A (earlier); false when no legal/within-limit merge exists.
-bool merge_ops(const Op& A, const Op& B, int fuse_k, Op& out) {
+bool merge_ops(const Op& A, const Op& B, int fuse_k, int min_low, int max_high, Op& out) {
     if (A.kind == OpKind::Fence || B.kind == OpKind::Fence || A.kind == OpKind::RBlock ||
         B.kind == OpKind::RBlock)
         return false;
@@ -247,6 +247,14 @@ bool merge_ops(const Op& A, const Op& B, int fuse_k, Op& out) {
     const int limit = both_diag ? QSV_MAX_DIAG_K : fuse_k;
     if (static_cast<int>(T.size()) > limit)
         return false;
+    if (!both_diag) {
+        // a dense block must fit one tile: at most max_high targets above the low run
+        int high = 0;
+        for (int q : T)
+            high += q >= min_low;
+        if (high > max_high)
+            return false;
+    }
     if (!both_diag && T.empty())
         return false;
     const std::size_t D = std::size_t{1} << T.size();
@@ -415,6 +423,8 @@ std::vector<Op> lower(const Circuit& c) {
 }
 
 std::vector<Op> fuse_ops(const std::vector<Op>& in, const PlanOptions& opt) {
+    const int min_low = opt.min_low;
+    const int max_high = std::min(QSV_MAX_HIGH, std::max(opt.tile_k - opt.min_low, 0));
     std::vector<Op> out;
     out.reserve(in.size());
     int nq = 0;
@@ -429,7 +439,7 @@ std::vector<Op> fuse_ops(const std::vector<Op>& in, const PlanOptions& opt) {
             a = std::max(a, frontier[q]);
         if (b.kind != OpKind::Fence && a >= 0 && out[a].kind != OpKind::Fence) {
             Op merged;
-            if (merge_ops(out[a], b, opt.fuse_k, merged) &&
+            if (merge_ops(out[a], b, opt.fuse_k, min_low, max_high, merged) &&
                 op_cost(merged) <= op_cost(out[a]) + op_cost(b) + 1e-9) {
                 out[a] = std::move(merged);
                 for (int q : footprint(out[a]))
@@ -451,7 +461,7 @@ std::vector<Op> fuse_ops(const std::vector<Op>& in, const PlanOptions& opt) {
     return kept;
 }
 
-std::vector<Op> form_blocks(const std::vector<Op>& in) {
+std::vector<Op> form_blocks(const std::vector<Op>& in, int min_low, int max_high) {
     struct Slot {
         Op op;                    // the op (or the first member while a block is open)
         std::vector<int> qubits;  // block footprint
@@ -474,7 +484,10 @@ std::vector<Op> form_blocks(const std::vector<Op>& in) {
                 for (int q : qb)
                     if (!contains(u, q))
                         u.push_back(q);
-                if (u.size() <= 4) {
+                int high = 0;
+                for (int q : u)
+                    high += q >= min_low;
+                if (u.size() <= 4 && high <= max_high) {
                     out[a].qubits = u;
                     out[a].members.push_back(b);
                     for (int q : u)
@@ -764,7 +777,10 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     std::vector<Op> ops = lower(c);
     plan.stats.ops_lowered = ops.size();
     if (opt.fusion) {
-        ops = fuse_ops(ops, opt);
+        PlanOptions fo = opt;
+        fo.tile_k = std::min(opt.tile_k, plan.n_local);
+        fo.min_low = std::min(opt.min_low, fo.tile_k);
+        ops = fuse_ops(ops, fo);
     } else {
         std::vector<Op> kept;
         for (Op& o : ops)
@@ -775,7 +791,7 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     plan.stats.ops_fused = ops.size();
     const int K = std::min(opt.tile_k, plan.n_local);
     if (opt.fusion && opt.register_blocks && K >= std::max(opt.min_low, 5) && opt.multi_op_passes)
-        ops = form_blocks(ops);
+        ops = form_blocks(ops, std::min(opt.min_low, K), std::min(QSV_MAX_HIGH, K - std::min(opt.min_low, K)));
     plan.stats.ops_final = ops.size();
     for (const Op& o : ops) {
         plan.stats.cost_units += op_cost(o);

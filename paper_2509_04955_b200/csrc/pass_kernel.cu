@@ -352,51 +352,59 @@ __device__ __forceinline__ void rb_u2(double2 (&v)[16], const double2* M) {
     }
 }
 
-template <int C, int T>  // X on T controlled by C
-__device__ __forceinline__ void rb_cx(double2 (&v)[16]) {
+// Registers hold the group in a per-lane rotated order: v[j] is member j ^ r.
+// A CX on (C, T) swaps members with bit C = 1, i.e. registers whose bit C
+// differs from r_C.
+template <int C, int T>
+__device__ __forceinline__ void rb_cx(double2 (&v)[16], uint32_t r) {
+    const bool rc = (r >> C) & 1u;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        if (!(j & (1 << C)) || (j & (1 << T)))
+        if (j & (1 << T))
             continue;
-        const double2 t = v[j];
-        v[j] = v[j | (1 << T)];
-        v[j | (1 << T)] = t;
+        const bool fire = (((j >> C) & 1) != 0) != rc;
+        const double2 x0 = v[j], x1 = v[j | (1 << T)];
+        v[j] = fire ? x1 : x0;
+        v[j | (1 << T)] = fire ? x0 : x1;
     }
 }
 
-__device__ __forceinline__ void rb_diag(double2 (&v)[16], const double2* D) {
+__device__ __forceinline__ void rb_diag(double2 (&v)[16], const double2* D, uint32_t r) {
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-        v[j] = cmul(D[j], v[j]);
+        v[j] = cmul(D[j ^ r], v[j]);
 }
 
 #define RB_CODE(kind, a, b) (((kind) << 4) | ((a) << 2) | (b))
 
-__device__ __forceinline__ void rb_apply(double2 (&v)[16], const DevPrim pr, const double2* m) {
+__device__ __forceinline__ void rb_apply(double2 (&v)[16], const DevPrim pr, const double2* m, uint32_t r) {
+    const uint32_t ra = (r >> pr.a) & 1u, rb = (r >> pr.b) & 1u;
+    const double2* m1 = m + 4 * ra;                 // U1 variant (U or XUX)
+    const double2* m2 = m + 16 * (ra | (rb << 1));  // U2 variant
     switch (RB_CODE(pr.kind, pr.a, pr.b)) {
-    case RB_CODE(QSV_PRIM_U1, 0, 0): rb_u1<0>(v, m); break;
-    case RB_CODE(QSV_PRIM_U1, 1, 0): rb_u1<1>(v, m); break;
-    case RB_CODE(QSV_PRIM_U1, 2, 0): rb_u1<2>(v, m); break;
-    case RB_CODE(QSV_PRIM_U1, 3, 0): rb_u1<3>(v, m); break;
-    case RB_CODE(QSV_PRIM_U2, 0, 1): rb_u2<0, 1>(v, m); break;
-    case RB_CODE(QSV_PRIM_U2, 0, 2): rb_u2<0, 2>(v, m); break;
-    case RB_CODE(QSV_PRIM_U2, 0, 3): rb_u2<0, 3>(v, m); break;
-    case RB_CODE(QSV_PRIM_U2, 1, 2): rb_u2<1, 2>(v, m); break;
-    case RB_CODE(QSV_PRIM_U2, 1, 3): rb_u2<1, 3>(v, m); break;
-    case RB_CODE(QSV_PRIM_U2, 2, 3): rb_u2<2, 3>(v, m); break;
-    case RB_CODE(QSV_PRIM_CX, 0, 1): rb_cx<0, 1>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 0, 2): rb_cx<0, 2>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 0, 3): rb_cx<0, 3>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 1, 0): rb_cx<1, 0>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 1, 2): rb_cx<1, 2>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 1, 3): rb_cx<1, 3>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 2, 0): rb_cx<2, 0>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 2, 1): rb_cx<2, 1>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 2, 3): rb_cx<2, 3>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 3, 0): rb_cx<3, 0>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 3, 1): rb_cx<3, 1>(v); break;
-    case RB_CODE(QSV_PRIM_CX, 3, 2): rb_cx<3, 2>(v); break;
-    default: rb_diag(v, m); break;  // QSV_PRIM_DIAG16
+    case RB_CODE(QSV_PRIM_U1, 0, 0): rb_u1<0>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1, 1, 0): rb_u1<1>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1, 2, 0): rb_u1<2>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1, 3, 0): rb_u1<3>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 1): rb_u2<0, 1>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 2): rb_u2<0, 2>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 3): rb_u2<0, 3>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 1, 2): rb_u2<1, 2>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 1, 3): rb_u2<1, 3>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 2, 3): rb_u2<2, 3>(v, m2); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 1): rb_cx<0, 1>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 2): rb_cx<0, 2>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 3): rb_cx<0, 3>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 0): rb_cx<1, 0>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 2): rb_cx<1, 2>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 3): rb_cx<1, 3>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 0): rb_cx<2, 0>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 1): rb_cx<2, 1>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 3): rb_cx<2, 3>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 3, 0): rb_cx<3, 0>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 3, 1): rb_cx<3, 1>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 3, 2): rb_cx<3, 2>(v, r); break;
+    default: rb_diag(v, m, r); break;  // QSV_PRIM_DIAG16
     }
 }
 
@@ -410,6 +418,9 @@ __device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const
     const uint32_t groups = 1u << (K - nfix);
     if (threadIdx.x >= groups)
         return;
+    // this lane's member rotation (bank spreading), as block bits and tile offset
+    const uint32_t r = (op.rot_tab >> (4 * (threadIdx.x & 7))) & 15u;
+    const uint32_t offr = ((r & 1) ? m0 : 0u) | ((r & 2) ? m1 : 0u) | ((r & 4) ? m2 : 0u) | ((r & 8) ? m3 : 0u);
     uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
     const uint32_t dstep = deposit(NT, op.fixpos, nfix);
     const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
@@ -417,21 +428,21 @@ __device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const
     const int np = op.nprim;
 #pragma unroll 1
     for (uint32_t st = 0; st < steps; ++st) {
-        const uint32_t idx = b | tctrl;
+        const uint32_t base = b | tctrl | offr;
         double2 v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-            v[j] = tile[idx | ((j & 1) ? m0 : 0u) | ((j & 2) ? m1 : 0u) | ((j & 4) ? m2 : 0u) |
-                        ((j & 8) ? m3 : 0u)];
+            v[j] = tile[base ^ (((j & 1) ? m0 : 0u) | ((j & 2) ? m1 : 0u) | ((j & 4) ? m2 : 0u) |
+                                ((j & 8) ? m3 : 0u))];
 #pragma unroll 1
         for (int p = 0; p < np; ++p) {
             const DevPrim pr = prims[p];
-            rb_apply(v, pr, reinterpret_cast<const double2*>(blob + pr.data_byte));
+            rb_apply(v, pr, reinterpret_cast<const double2*>(blob + pr.data_byte), r);
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-            tile[idx | ((j & 1) ? m0 : 0u) | ((j & 2) ? m1 : 0u) | ((j & 4) ? m2 : 0u) |
-                 ((j & 8) ? m3 : 0u)] = v[j];
+            tile[base ^ (((j & 1) ? m0 : 0u) | ((j & 2) ? m1 : 0u) | ((j & 4) ? m2 : 0u) |
+                         ((j & 8) ? m3 : 0u))] = v[j];
         b = next_group(b, F, dstep);
     }
 }

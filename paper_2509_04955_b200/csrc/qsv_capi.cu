@@ -552,13 +552,25 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                 default:
                     QSV_REQUIRE(false, "prim: unknown RBLOCK primitive kind");
                 }
+                std::vector<double> d;
                 if (ne) {
                     QSV_REQUIRE(pd.mat_off >= 0 && static_cast<size_t>(pd.mat_off) + ne <= pool_len,
                                 "prim: matrix outside the pool");
-                    pl.pdata.emplace_back(pool + 2 * pd.mat_off, pool + 2 * (pd.mat_off + ne));
-                } else {
-                    pl.pdata.emplace_back();
+                    const double* m = pool + 2 * pd.mat_off;
+                    if (pd.kind == QSV_PRIM_U1 || pd.kind == QSV_PRIM_U2) {
+                        // rotation variants: M_s[i][j] = M[i ^ s][j ^ s]
+                        const int dim = pd.kind == QSV_PRIM_U1 ? 2 : 4;
+                        for (int sv = 0; sv < dim; ++sv)
+                            for (int i = 0; i < dim; ++i)
+                                for (int j = 0; j < dim; ++j) {
+                                    d.push_back(m[2 * ((i ^ sv) * dim + (j ^ sv))]);
+                                    d.push_back(m[2 * ((i ^ sv) * dim + (j ^ sv)) + 1]);
+                                }
+                    } else {
+                        d.assign(m, m + 2 * ne);
+                    }
                 }
+                pl.pdata.push_back(std::move(d));
                 pl.dprims.push_back(dp);
                 flops += fl * amps * frac;
             }
@@ -650,6 +662,29 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
         }
         std::sort(fix.begin(), fix.end());
         QSV_REQUIRE(fix.size() <= sizeof(t.fixpos), "op: too many fixed tile bits");
+        if (od.kind == QSV_OP_RBLOCK) {
+            // Lanes i = 0..7 of a quarter-warp own groups whose low free bits are
+            // the lowest free tile positions.  The first `a` of them lie in tile
+            // bits 0..2 (the SMEM bank bits of 16-B amplitudes); lanes that differ
+            // only in the next bits would hit the same banks, so their member
+            // order is rotated by XOR over the block slots sitting in bits 0..2.
+            std::vector<int> lowslots;
+            for (int sl = 0; sl < 4; ++sl)
+                if (t.tpos[sl] < 3)
+                    lowslots.push_back(sl);
+            int a = 0;
+            for (int pbit = 0; pbit < 3 && pbit < K; ++pbit)
+                if (std::find(fix.begin(), fix.end(), pbit) == fix.end())
+                    ++a;
+            for (int i = 0; i < 8; ++i) {
+                const int hi = i >> a;
+                uint32_t r = 0;
+                for (size_t j = 0; j < lowslots.size(); ++j)
+                    if (hi >> j & 1)
+                        r |= 1u << lowslots[j];
+                t.rot_tab |= r << (4 * i);
+            }
+        }
         t.nfix = static_cast<int32_t>(fix.size());
         for (size_t i = 0; i < fix.size(); ++i) {
             t.fixpos[i] = static_cast<int8_t>(fix[i]);

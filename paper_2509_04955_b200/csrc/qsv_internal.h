@@ -34,6 +34,8 @@ struct TileOp {
     uint32_t ptab_byte;           // DIAG: byte offset of pext tables (uint8 [32] low, [64] high)
     uint32_t prim_byte;           // RBLOCK: DevPrim list; PHASEPROD: ExtFactor list
     int32_t nprim;
+    uint32_t rot_tab;             // RBLOCK: 4-bit member rotation per lane & 7 (bank spreading)
+    uint32_t pad2[3];
 };
 
 // RBLOCK primitive as stored in the blob.
@@ -41,7 +43,9 @@ struct DevPrim {
     uint8_t kind;       // QSV_PRIM_U1 / U2 / CX / DIAG16
     uint8_t a, b;       // block-local qubit indices (0..3)
     uint8_t pad;
-    uint32_t data_byte; // blob offset of the matrix / table
+    uint32_t data_byte; // blob offset of the matrix / table; U1 stores 2 variants
+                        // (U, XUX), U2 stores 4 (conjugated by X on a, b), one per
+                        // member rotation of the lane
 };
 
 // PHASEPROD factor on a qubit outside the tile (CTA-uniform).
