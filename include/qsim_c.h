@@ -44,6 +44,8 @@ typedef struct qsim_plan_opts {
     int32_t nbuf;             /* BBOP buffers B                                 */
     int32_t register_blocks;  /* group native gates on <= 4 qubits (RBLOCK)     */
     double pass_budget;       /* DP cost units per amplitude per pass           */
+    int32_t rblock_k;         /* register-block width: 3 or 4 qubits            */
+    int32_t reserved;
 } qsim_plan_opts;
 
 typedef struct qsim_plan_stats {

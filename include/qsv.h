@@ -112,8 +112,9 @@ int qsv_apply_fused(qsv_state* st, int k, const int* targets, uint64_t ctrl_mask
 #define QSV_OP_DIAG 1   /* diagonal of 2^k entries on k qubits (any, incl. global) */
 #define QSV_OP_XPERM 2  /* Pauli-X permutation on one LOCAL target (+ controls)    */
 #define QSV_OP_RBLOCK 3 /* register block: a list of primitives (U1/U2/CX/DIAG16) on
-                         * 4 LOCAL tile qubits qubits[0..3], applied to each 16-amplitude
-                         * group in registers (one SMEM round trip for the whole list) */
+                         * k = 3 or 4 LOCAL tile qubits qubits[0..k), applied to each
+                         * 2^k-amplitude group in registers (one SMEM round trip for
+                         * the whole list) */
 #define QSV_OP_PHASEPROD 4 /* separable phase product: for amplitudes with all ctrl_mask
                          * bits set, multiply by pool[mat_off] * prod over FACTOR
                          * primitives (qubit q set) of pool[prim.mat_off]; qubits
@@ -124,8 +125,10 @@ int qsv_apply_fused(qsv_state* st, int k, const int* targets, uint64_t ctrl_mask
 #define QSV_PRIM_U1 0      /* 2x2 on block qubit a                                   */
 #define QSV_PRIM_U2 1      /* 4x4 on block qubits (a, b), a < b, a = low matrix bit   */
 #define QSV_PRIM_CX 2      /* X on block qubit b controlled by block qubit a          */
-#define QSV_PRIM_DIAG16 3  /* 16-entry diagonal over the 4 block qubits (bit i = qubits[i]) */
+#define QSV_PRIM_DIAG16 3  /* 2^k-entry diagonal over the k block qubits (bit i = qubits[i]) */
 #define QSV_PRIM_FACTOR 4  /* PHASEPROD factor: multiply when physical qubit a is 1    */
+#define QSV_PRIM_U1R 5     /* 2x2 with real entries (H, RY): 4 DFMA per amplitude     */
+#define QSV_PRIM_U1I 6     /* 2x2 real diagonal, imaginary off-diagonal (RX)          */
 
 typedef struct qsv_prim_desc {
     int32_t kind;

@@ -54,6 +54,8 @@ class qsim_plan_opts(C.Structure):
         ("nbuf", C.c_int32),
         ("register_blocks", C.c_int32),
         ("pass_budget", C.c_double),
+        ("rblock_k", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -138,18 +140,19 @@ class PlanOptions:
     nbuf: int = 2
     pass_budget: float = 72.0
     register_blocks: bool = True
+    rblock_k: int = 4
 
     @classmethod
     def default(cls) -> "PlanOptions":
         o = qsim_plan_opts()
         load_qsim().qsim_default_opts(C.byref(o))
         return cls(o.tile_k, o.min_low, o.fuse_k, bool(o.fusion), bool(o.multi_op_passes),
-                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks))
+                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k)
 
     def to_c(self) -> qsim_plan_opts:
         return qsim_plan_opts(self.tile_k, self.min_low, self.fuse_k, int(self.fusion),
                               int(self.multi_op_passes), self.chunk_log2, self.nbuf,
-                              int(self.register_blocks), float(self.pass_budget))
+                              int(self.register_blocks), float(self.pass_budget), int(self.rblock_k), 0)
 
 
 class Circuit:

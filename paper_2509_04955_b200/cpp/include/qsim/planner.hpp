@@ -47,6 +47,7 @@ struct Op {
                                 // PhaseProd: data[0] = constant factor
     std::vector<std::pair<int, Amp>> factors;  // PhaseProd: multiply by f when qubit is 1
     std::vector<Prim> prims;    // RBlock
+    int width = 0;              // RBlock: register-block width (3 or 4 slots)
     int first_gate = -1;        // provenance (gate index range)
     int last_gate = -1;
     int ngates = 0;             // source gates merged into this op
@@ -56,7 +57,8 @@ struct PlanOptions {
     int tile_k = 11;          // tile qubits per pass (<= 11)
     int min_low = 5;          // contiguous low run: 2^5 amplitudes = 512-B DRAM runs
     int fuse_k = 2;           // largest dense block fusion may create (<= QSV_MAX_DENSE_K)
-    bool register_blocks = true;  // group native gates on <= 4 qubits into RBLOCK ops
+    bool register_blocks = true;  // group native gates on <= rblock_k qubits into RBLOCK ops
+    int rblock_k = 4;         // register-block width: 3 (8 amplitudes/thread) or 4 (16)
     bool fusion = true;       // DAGC on/off (BASELINE configs[1]: "contraction on vs off")
     bool multi_op_passes = true;  // SMGP on/off: off = one op per pass
     double pass_budget = 72;  // DP cost units per amplitude allowed in one pass
@@ -92,7 +94,7 @@ std::vector<Op> lower(const Circuit& c);
 std::vector<Op> fuse_ops(const std::vector<Op>& ops, const PlanOptions& opt);
 // Groups ops acting on <= 4 qubits into register blocks (RBLOCK); a block holds
 // at most max_high qubits at or above min_low (it must fit one pass tile).
-std::vector<Op> form_blocks(const std::vector<Op>& ops, int min_low = 5, int max_high = 6);
+std::vector<Op> form_blocks(const std::vector<Op>& ops, int min_low = 5, int max_high = 5, int width = 3);
 // Relative DP cost per amplitude of one op (the packing / fusion currency).
 double op_cost(const Op& op);
 // Builds the full plan (lower -> fuse -> partition/swaps -> pack).

@@ -56,6 +56,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.chunk_log2 = o->chunk_log2;
     p.nbuf = o->nbuf;
     p.pass_budget = o->pass_budget;
+    p.rblock_k = o->rblock_k;
     return p;
 }
 
@@ -107,6 +108,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->chunk_log2 = p.chunk_log2;
     out->nbuf = p.nbuf;
     out->pass_budget = p.pass_budget;
+    out->rblock_k = p.rblock_k;
 }
 
 int qsim_circuit_generate(const char* spec, qsim_circuit** out) {
@@ -217,7 +219,7 @@ int qsim_circuit_fused(const qsim_circuit* c, const qsim_plan_opts* opts, qsim_c
         if (o.fusion) {
             ops = qsim::fuse_ops(ops, o);
             if (o.register_blocks)
-                ops = qsim::form_blocks(ops, o.min_low, std::max(o.tile_k - o.min_low, 0));
+                ops = qsim::form_blocks(ops, o.min_low, std::max(o.tile_k - o.min_low, 0), o.rblock_k);
         }
         std::vector<qsim::Op> kept;
         for (auto& op : ops)

@@ -308,18 +308,20 @@ bool is_identity(const Op& o) {
 }
 
 // ------------------------------------------------------------ register blocks
-bool block_eligible(const Op& o) {
+bool block_eligible(const Op& o, int width) {
     switch (o.kind) {
     case OpKind::Dense: return o.qubits.size() + o.controls.size() <= 2;
     case OpKind::XPerm: return o.controls.size() <= 1;
     case OpKind::Diag:
-    case OpKind::PhaseProd: return footprint(o).size() <= 4;
+    case OpKind::PhaseProd: return static_cast<int>(footprint(o).size()) <= width;
     default: return false;
     }
 }
 
 double prim_cost(const Prim& p) {
     switch (p.kind) {
+    case QSV_PRIM_U1R:
+    case QSV_PRIM_U1I: return 4.0;
     case QSV_PRIM_U1: return 8.0;
     case QSV_PRIM_U2: return 16.0;
     case QSV_PRIM_CX: return 0.5;
@@ -328,18 +330,20 @@ double prim_cost(const Prim& p) {
 }
 
 // Converts the member ops of a block (qubits sorted = slots) into primitives.
-std::vector<Prim> block_prims(const std::vector<int>& slots, const std::vector<Op>& members) {
+// Diagonal tables are laid out over 2^width entries (padded slots repeat).
+std::vector<Prim> block_prims(const std::vector<int>& slots, const std::vector<Op>& members, int width) {
+    const int ND = 1 << width;
     std::vector<Prim> out;
     auto slot = [&](int q) { return index_of(slots, q); };
     for (const Op& o : members) {
         Prim p;
         if (diag_like(o)) {
             p.kind = QSV_PRIM_DIAG16;
-            p.data.resize(16);
-            for (int e = 0; e < 16; ++e)
+            p.data.resize(ND);
+            for (int e = 0; e < ND; ++e)
                 p.data[e] = diag_value(o, [&](int q) { return (e >> slot(q)) & 1; });
             if (!out.empty() && out.back().kind == QSV_PRIM_DIAG16) {
-                for (int e = 0; e < 16; ++e)
+                for (int e = 0; e < ND; ++e)
                     out.back().data[e] = p.data[e] * out.back().data[e];
                 continue;
             }
@@ -364,6 +368,16 @@ std::vector<Prim> block_prims(const std::vector<int>& slots, const std::vector<O
             p.data = expand_dense(o, fp);
         }
         out.push_back(std::move(p));
+    }
+    // structured 2x2 primitives: half the DFMA work of a general complex 2x2
+    for (Prim& p : out) {
+        if (p.kind != QSV_PRIM_U1)
+            continue;
+        const auto& m = p.data;
+        if (m[0].imag() == 0 && m[1].imag() == 0 && m[2].imag() == 0 && m[3].imag() == 0)
+            p.kind = QSV_PRIM_U1R;
+        else if (m[0].imag() == 0 && m[3].imag() == 0 && m[1].real() == 0 && m[2].real() == 0)
+            p.kind = QSV_PRIM_U1I;
     }
     return out;
 }
@@ -461,68 +475,106 @@ std::vector<Op> fuse_ops(const std::vector<Op>& in, const PlanOptions& opt) {
     return kept;
 }
 
-std::vector<Op> form_blocks(const std::vector<Op>& in, int min_low, int max_high) {
-    struct Slot {
-        Op op;                    // the op (or the first member while a block is open)
-        std::vector<int> qubits;  // block footprint
-        std::vector<Op> members;  // > 1 when it became a block
-    };
-    std::vector<Slot> out;
+std::vector<Op> form_blocks(const std::vector<Op>& in, int min_low, int max_high, int width) {
+    // Greedy register blocking over the dependency DAG: a block starts at the
+    // earliest unprocessed op and repeatedly absorbs any *available* op (every
+    // earlier op on its qubits already placed) whose qubits keep the block within
+    // `width` qubits (and within `max_high` qubits above the tile's low run).
+    // Ops are emitted in block order, which respects every dependency.
+    const int nops = static_cast<int>(in.size());
     int nq = 0;
-    for (const Op& o : in)
-        for (int q : footprint(o))
+    std::vector<std::vector<int>> fp(nops);
+    for (int i = 0; i < nops; ++i) {
+        fp[i] = footprint(in[i]);
+        for (int q : fp[i])
             nq = std::max(nq, q + 1);
-    std::vector<int> frontier(static_cast<std::size_t>(nq), -1);
-    for (const Op& b : in) {
-        const std::vector<int> qb = footprint(b);
-        if (block_eligible(b)) {
-            int a = -1;
-            for (int q : qb)
-                a = std::max(a, frontier[q]);
-            if (a >= 0 && !out[a].members.empty()) {
-                std::vector<int> u = out[a].qubits;
-                for (int q : qb)
-                    if (!contains(u, q))
-                        u.push_back(q);
-                int high = 0;
-                for (int q : u)
-                    high += q >= min_low;
-                if (u.size() <= 4 && high <= max_high) {
-                    out[a].qubits = u;
-                    out[a].members.push_back(b);
-                    for (int q : u)
-                        frontier[q] = std::max(frontier[q], a);
+    }
+    std::vector<std::vector<int>> on_qubit(nq);
+    for (int i = 0; i < nops; ++i)
+        for (int q : fp[i])
+            on_qubit[q].push_back(i);
+    std::vector<std::size_t> next(nq, 0);
+    std::vector<char> done(nops, 0);
+    auto available = [&](int i) {
+        for (int q : fp[i])
+            if (next[q] >= on_qubit[q].size() || on_qubit[q][next[q]] != i)
+                return false;
+        return true;
+    };
+    auto take = [&](int i) {
+        done[i] = 1;
+        for (int q : fp[i])
+            ++next[q];
+    };
+    auto high_count = [&](const std::vector<int>& u) {
+        int h = 0;
+        for (int q : u)
+            h += q >= min_low;
+        return h;
+    };
+    std::vector<Op> res;
+    res.reserve(in.size());
+    int cursor = 0;
+    while (true) {
+        while (cursor < nops && done[cursor])
+            ++cursor;
+        if (cursor >= nops)
+            break;
+        const int g0 = cursor;  // earliest unprocessed op: always available
+        if (!block_eligible(in[g0], width) || high_count(fp[g0]) > max_high) {
+            take(g0);
+            res.push_back(in[g0]);
+            continue;
+        }
+        std::vector<int> S = fp[g0];
+        std::vector<int> members = {g0};
+        take(g0);
+        while (true) {
+            int best = -1, best_growth = 1 << 20;
+            std::vector<int> best_u;
+            for (int q = 0; q < nq; ++q) {
+                if (next[q] >= on_qubit[q].size())
                     continue;
+                const int i = on_qubit[q][next[q]];
+                if (done[i] || !available(i) || !block_eligible(in[i], width))
+                    continue;
+                std::vector<int> u = S;
+                for (int x : fp[i])
+                    if (!contains(u, x))
+                        u.push_back(x);
+                if (static_cast<int>(u.size()) > width || high_count(u) > max_high)
+                    continue;
+                const int growth = static_cast<int>(u.size() - S.size());
+                if (growth < best_growth || (growth == best_growth && i < best)) {
+                    best = i;
+                    best_growth = growth;
+                    best_u = u;
                 }
             }
-            Slot s;
-            s.op = b;
-            s.qubits = qb;
-            s.members.push_back(b);
-            out.push_back(std::move(s));
-        } else {
-            Slot s;
-            s.op = b;
-            out.push_back(std::move(s));
+            if (best < 0)
+                break;
+            S = best_u;
+            members.push_back(best);
+            take(best);
         }
-        for (int q : qb)
-            frontier[q] = static_cast<int>(out.size()) - 1;
-    }
-    std::vector<Op> res;
-    res.reserve(out.size());
-    for (Slot& s : out) {
-        if (s.members.size() <= 1) {
-            res.push_back(std::move(s.op));
+        const Op& first = in[members[0]];
+        const bool single_diag = members.size() == 1 && (diag_like(first) || first.kind == OpKind::XPerm);
+        if (single_diag) {
+            res.push_back(first);
             continue;
         }
         Op blk;
         blk.kind = OpKind::RBlock;
-        blk.qubits = s.qubits;
+        blk.qubits = S;
         std::sort(blk.qubits.begin(), blk.qubits.end());
-        blk.prims = block_prims(blk.qubits, s.members);
-        blk.first_gate = s.members.front().first_gate;
-        blk.last_gate = s.members.back().last_gate;
-        for (const Op& m : s.members)
+        std::vector<Op> mops;
+        for (int m : members)
+            mops.push_back(in[m]);
+        blk.prims = block_prims(blk.qubits, mops, width);
+        blk.width = width;
+        blk.first_gate = in[members.front()].first_gate;
+        blk.last_gate = in[members.back()].last_gate;
+        for (const Op& m : mops)
             blk.ngates += m.ngates;
         res.push_back(std::move(blk));
     }
@@ -610,7 +662,8 @@ struct Packer {
         std::vector<int> phys;
         for (int q : o.qubits)
             phys.push_back(pos[q]);
-        for (int p = 0; phys.size() < 4 && p < Lmin; ++p)
+        const std::size_t width = static_cast<std::size_t>(o.width);
+        for (int p = 0; phys.size() < width && p < Lmin; ++p)
             if (!contains(phys, p))
                 phys.push_back(p);
         return phys;
@@ -659,9 +712,9 @@ struct Packer {
             break;
         case OpKind::RBlock: {
             d.kind = QSV_OP_RBLOCK;
-            d.k = 4;
             const std::vector<int> phys = block_slots(o);
-            for (int i = 0; i < 4; ++i)
+            d.k = static_cast<int>(phys.size());
+            for (int i = 0; i < d.k; ++i)
                 d.qubits[i] = phys[i];
             d.prim_begin = static_cast<int>(plan.prims.size());
             // slot data is laid out over the block's own qubits (slots 0..|q|-1);
@@ -672,11 +725,7 @@ struct Packer {
                 p.a = pr.a;
                 p.b = pr.b;
                 if (pr.kind == QSV_PRIM_DIAG16) {
-                    std::vector<Amp> t(16);
-                    const int nb = static_cast<int>(o.qubits.size());
-                    for (int e = 0; e < 16; ++e)
-                        t[e] = pr.data[e & ((1 << nb) - 1)];
-                    p.mat_off = put(t);
+                    p.mat_off = put(pr.data);
                 } else if (!pr.data.empty()) {
                     p.mat_off = put(pr.data);
                 }
@@ -768,6 +817,8 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
         throw std::invalid_argument("make_plan: fuse_k must be in [1, 5]");
     if (opt.tile_k < 1 || opt.tile_k > 11)
         throw std::invalid_argument("make_plan: tile_k must be in [1, 11]");
+    if (opt.rblock_k != 3 && opt.rblock_k != 4)
+        throw std::invalid_argument("make_plan: rblock_k must be 3 or 4");
     Plan plan;
     plan.n = c.n;
     plan.n_local = opt.n_local < 0 ? c.n : opt.n_local;
@@ -791,7 +842,8 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     plan.stats.ops_fused = ops.size();
     const int K = std::min(opt.tile_k, plan.n_local);
     if (opt.fusion && opt.register_blocks && K >= std::max(opt.min_low, 5) && opt.multi_op_passes)
-        ops = form_blocks(ops, std::min(opt.min_low, K), std::min(QSV_MAX_HIGH, K - std::min(opt.min_low, K)));
+        ops = form_blocks(ops, std::min(opt.min_low, K), std::min(QSV_MAX_HIGH, K - std::min(opt.min_low, K)),
+                          opt.rblock_k);
     plan.stats.ops_final = ops.size();
     for (const Op& o : ops) {
         plan.stats.cost_units += op_cost(o);
@@ -919,7 +971,7 @@ Circuit ops_to_circuit(int n, const std::vector<Op>& ops) {
         case OpKind::RBlock:
             for (const Prim& p : o.prims) {
                 const std::vector<int>& s = o.qubits;
-                if (p.kind == QSV_PRIM_U1) {
+                if (p.kind == QSV_PRIM_U1 || p.kind == QSV_PRIM_U1R || p.kind == QSV_PRIM_U1I) {
                     add_matrix({s[p.a]}, {}, p.data);
                 } else if (p.kind == QSV_PRIM_U2) {
                     add_matrix({s[p.a], s[p.b]}, {}, p.data);

@@ -305,15 +305,17 @@ __device__ __forceinline__ void dense5_op(double2* tile, const TileOp& op, const
 }
 
 // ---------------------------------------------------------------- RBLOCK
-// A register block holds one 16-amplitude group (4 block qubits) per thread and
-// applies a list of native gates to it in registers; the list is uniform over
-// the CTA, so the per-primitive switch is a uniform branch.  Amplitude j of the
-// group has block-qubit i in bit i of j.
-template <int Q>
-__device__ __forceinline__ void rb_u1(double2 (&v)[16], const double2* U) {
+// A register block holds one group of NV = 2^KB amplitudes (KB = 3 or 4 block
+// qubits) per thread and applies a list of native gates to it in registers;
+// the list is uniform over the CTA, so the per-primitive switch is a uniform
+// branch.  Register v[j] holds group member j ^ r, where r is this lane's
+// member rotation (it spreads the lanes of a quarter-warp over the SMEM
+// banks); the host stores every matrix in its rotated variants.
+template <int NV, int Q>
+__device__ __forceinline__ void rb_u1(double2 (&v)[NV], const double2* U) {
     const double2 u00 = U[0], u01 = U[1], u10 = U[2], u11 = U[3];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < NV; ++j) {
         if (j & (1 << Q))
             continue;
         const double2 x0 = v[j], x1 = v[j | (1 << Q)];
@@ -327,10 +329,39 @@ __device__ __forceinline__ void rb_u1(double2 (&v)[16], const double2* U) {
     }
 }
 
-template <int A, int B>  // A < B: matrix bit 0 <-> block qubit A, bit 1 <-> B
-__device__ __forceinline__ void rb_u2(double2 (&v)[16], const double2* M) {
+// Real 2x2 (H, RY, products of them): the real and imaginary parts of the
+// amplitudes are transformed independently, 4 DFMA per amplitude.
+template <int NV, int Q>
+__device__ __forceinline__ void rb_u1r(double2 (&v)[NV], const double2* U) {
+    const double u00 = U[0].x, u01 = U[1].x, u10 = U[2].x, u11 = U[3].x;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < NV; ++j) {
+        if (j & (1 << Q))
+            continue;
+        const double2 x0 = v[j], x1 = v[j | (1 << Q)];
+        v[j] = make_double2(fma(u00, x0.x, u01 * x1.x), fma(u00, x0.y, u01 * x1.y));
+        v[j | (1 << Q)] = make_double2(fma(u10, x0.x, u11 * x1.x), fma(u10, x0.y, u11 * x1.y));
+    }
+}
+
+// Real diagonal, imaginary off-diagonal 2x2 (RX): [[c0, i s01], [i s10, c1]].
+template <int NV, int Q>
+__device__ __forceinline__ void rb_u1i(double2 (&v)[NV], const double2* U) {
+    const double c0 = U[0].x, s01 = U[1].y, s10 = U[2].y, c1 = U[3].x;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (j & (1 << Q))
+            continue;
+        const double2 x0 = v[j], x1 = v[j | (1 << Q)];
+        v[j] = make_double2(fma(c0, x0.x, -s01 * x1.y), fma(c0, x0.y, s01 * x1.x));
+        v[j | (1 << Q)] = make_double2(fma(c1, x1.x, -s10 * x0.y), fma(c1, x1.y, s10 * x0.x));
+    }
+}
+
+template <int NV, int A, int B>  // A < B: matrix bit 0 <-> block qubit A, bit 1 <-> B
+__device__ __forceinline__ void rb_u2(double2 (&v)[NV], const double2* M) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
         if (j & ((1 << A) | (1 << B)))
             continue;
         const int i1 = j | (1 << A), i2 = j | (1 << B), i3 = j | (1 << A) | (1 << B);
@@ -352,14 +383,13 @@ __device__ __forceinline__ void rb_u2(double2 (&v)[16], const double2* M) {
     }
 }
 
-// Registers hold the group in a per-lane rotated order: v[j] is member j ^ r.
-// A CX on (C, T) swaps members with bit C = 1, i.e. registers whose bit C
-// differs from r_C.
-template <int C, int T>
-__device__ __forceinline__ void rb_cx(double2 (&v)[16], uint32_t r) {
+// CX on (C, T) swaps members with bit C = 1, i.e. registers whose bit C
+// differs from the rotation bit r_C.
+template <int NV, int C, int T>
+__device__ __forceinline__ void rb_cx(double2 (&v)[NV], uint32_t r) {
     const bool rc = (r >> C) & 1u;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < NV; ++j) {
         if (j & (1 << T))
             continue;
         const bool fire = (((j >> C) & 1) != 0) != rc;
@@ -369,49 +399,69 @@ __device__ __forceinline__ void rb_cx(double2 (&v)[16], uint32_t r) {
     }
 }
 
-__device__ __forceinline__ void rb_diag(double2 (&v)[16], const double2* D, uint32_t r) {
+template <int NV>
+__device__ __forceinline__ void rb_diag(double2 (&v)[NV], const double2* D, uint32_t r) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < NV; ++j)
         v[j] = cmul(D[j ^ r], v[j]);
 }
 
 #define RB_CODE(kind, a, b) (((kind) << 4) | ((a) << 2) | (b))
 
-__device__ __forceinline__ void rb_apply(double2 (&v)[16], const DevPrim pr, const double2* m, uint32_t r) {
+template <int NV>
+__device__ __forceinline__ void rb_apply(double2 (&v)[NV], const DevPrim pr, const double2* m, uint32_t r) {
     const uint32_t ra = (r >> pr.a) & 1u, rb = (r >> pr.b) & 1u;
     const double2* m1 = m + 4 * ra;                 // U1 variant (U or XUX)
     const double2* m2 = m + 16 * (ra | (rb << 1));  // U2 variant
     switch (RB_CODE(pr.kind, pr.a, pr.b)) {
-    case RB_CODE(QSV_PRIM_U1, 0, 0): rb_u1<0>(v, m1); break;
-    case RB_CODE(QSV_PRIM_U1, 1, 0): rb_u1<1>(v, m1); break;
-    case RB_CODE(QSV_PRIM_U1, 2, 0): rb_u1<2>(v, m1); break;
-    case RB_CODE(QSV_PRIM_U1, 3, 0): rb_u1<3>(v, m1); break;
-    case RB_CODE(QSV_PRIM_U2, 0, 1): rb_u2<0, 1>(v, m2); break;
-    case RB_CODE(QSV_PRIM_U2, 0, 2): rb_u2<0, 2>(v, m2); break;
-    case RB_CODE(QSV_PRIM_U2, 0, 3): rb_u2<0, 3>(v, m2); break;
-    case RB_CODE(QSV_PRIM_U2, 1, 2): rb_u2<1, 2>(v, m2); break;
-    case RB_CODE(QSV_PRIM_U2, 1, 3): rb_u2<1, 3>(v, m2); break;
-    case RB_CODE(QSV_PRIM_U2, 2, 3): rb_u2<2, 3>(v, m2); break;
-    case RB_CODE(QSV_PRIM_CX, 0, 1): rb_cx<0, 1>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 0, 2): rb_cx<0, 2>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 0, 3): rb_cx<0, 3>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 1, 0): rb_cx<1, 0>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 1, 2): rb_cx<1, 2>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 1, 3): rb_cx<1, 3>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 2, 0): rb_cx<2, 0>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 2, 1): rb_cx<2, 1>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 2, 3): rb_cx<2, 3>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 3, 0): rb_cx<3, 0>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 3, 1): rb_cx<3, 1>(v, r); break;
-    case RB_CODE(QSV_PRIM_CX, 3, 2): rb_cx<3, 2>(v, r); break;
-    default: rb_diag(v, m, r); break;  // QSV_PRIM_DIAG16
+    case RB_CODE(QSV_PRIM_U1, 0, 0): rb_u1<NV, 0>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1, 1, 0): rb_u1<NV, 1>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1, 2, 0): rb_u1<NV, 2>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1R, 0, 0): rb_u1r<NV, 0>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1R, 1, 0): rb_u1r<NV, 1>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1R, 2, 0): rb_u1r<NV, 2>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1I, 0, 0): rb_u1i<NV, 0>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1I, 1, 0): rb_u1i<NV, 1>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1I, 2, 0): rb_u1i<NV, 2>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 1): rb_u2<NV, 0, 1>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 2): rb_u2<NV, 0, 2>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 1, 2): rb_u2<NV, 1, 2>(v, m2); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 1): rb_cx<NV, 0, 1>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 2): rb_cx<NV, 0, 2>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 0): rb_cx<NV, 1, 0>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 2): rb_cx<NV, 1, 2>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 0): rb_cx<NV, 2, 0>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 1): rb_cx<NV, 2, 1>(v, r); break;
+    default:
+        if constexpr (NV == 16) {
+            switch (RB_CODE(pr.kind, pr.a, pr.b)) {
+            case RB_CODE(QSV_PRIM_U1, 3, 0): rb_u1<NV, 3>(v, m1); return;
+            case RB_CODE(QSV_PRIM_U1R, 3, 0): rb_u1r<NV, 3>(v, m1); return;
+            case RB_CODE(QSV_PRIM_U1I, 3, 0): rb_u1i<NV, 3>(v, m1); return;
+            case RB_CODE(QSV_PRIM_U2, 0, 3): rb_u2<NV, 0, 3>(v, m2); return;
+            case RB_CODE(QSV_PRIM_U2, 1, 3): rb_u2<NV, 1, 3>(v, m2); return;
+            case RB_CODE(QSV_PRIM_U2, 2, 3): rb_u2<NV, 2, 3>(v, m2); return;
+            case RB_CODE(QSV_PRIM_CX, 0, 3): rb_cx<NV, 0, 3>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 1, 3): rb_cx<NV, 1, 3>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 2, 3): rb_cx<NV, 2, 3>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 3, 0): rb_cx<NV, 3, 0>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 3, 1): rb_cx<NV, 3, 1>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 3, 2): rb_cx<NV, 3, 2>(v, r); return;
+            default: break;
+            }
+        }
+        rb_diag<NV>(v, m, r);  // QSV_PRIM_DIAG16: 2^KB-entry diagonal
+        break;
     }
 }
 
-template <int K, int NT>
+template <int K, int NT, int KB>
 __device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const unsigned char* blob) {
-    const uint32_t m0 = 1u << op.tpos[0], m1 = 1u << op.tpos[1];
-    const uint32_t m2 = 1u << op.tpos[2], m3 = 1u << op.tpos[3];
+    constexpr int NV = 1 << KB;
+    uint32_t mk[KB];
+#pragma unroll
+    for (int i = 0; i < KB; ++i)
+        mk[i] = 1u << op.tpos[i];
     const int nfix = op.nfix;
     const uint32_t tctrl = op.tctrl;
     const uint32_t F = op.fmask;
@@ -420,7 +470,10 @@ __device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const
         return;
     // this lane's member rotation (bank spreading), as block bits and tile offset
     const uint32_t r = (op.rot_tab >> (4 * (threadIdx.x & 7))) & 15u;
-    const uint32_t offr = ((r & 1) ? m0 : 0u) | ((r & 2) ? m1 : 0u) | ((r & 4) ? m2 : 0u) | ((r & 8) ? m3 : 0u);
+    uint32_t offr = 0;
+#pragma unroll
+    for (int i = 0; i < KB; ++i)
+        offr |= ((r >> i) & 1u) ? mk[i] : 0u;
     uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
     const uint32_t dstep = deposit(NT, op.fixpos, nfix);
     const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
@@ -429,20 +482,28 @@ __device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const
 #pragma unroll 1
     for (uint32_t st = 0; st < steps; ++st) {
         const uint32_t base = b | tctrl | offr;
-        double2 v[16];
+        double2 v[NV];
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            v[j] = tile[base ^ (((j & 1) ? m0 : 0u) | ((j & 2) ? m1 : 0u) | ((j & 4) ? m2 : 0u) |
-                                ((j & 8) ? m3 : 0u))];
+        for (int j = 0; j < NV; ++j) {
+            uint32_t o = 0;
+#pragma unroll
+            for (int i = 0; i < KB; ++i)
+                o |= ((j >> i) & 1) ? mk[i] : 0u;
+            v[j] = tile[base ^ o];
+        }
 #pragma unroll 1
         for (int p = 0; p < np; ++p) {
             const DevPrim pr = prims[p];
-            rb_apply(v, pr, reinterpret_cast<const double2*>(blob + pr.data_byte), r);
+            rb_apply<NV>(v, pr, reinterpret_cast<const double2*>(blob + pr.data_byte), r);
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-            tile[base ^ (((j & 1) ? m0 : 0u) | ((j & 2) ? m1 : 0u) | ((j & 4) ? m2 : 0u) |
-                         ((j & 8) ? m3 : 0u))] = v[j];
+        for (int j = 0; j < NV; ++j) {
+            uint32_t o = 0;
+#pragma unroll
+            for (int i = 0; i < KB; ++i)
+                o |= ((j >> i) & 1) ? mk[i] : 0u;
+            tile[base ^ o] = v[j];
+        }
         b = next_group(b, F, dstep);
     }
 }
@@ -498,7 +559,7 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const GeomArg& g) {
 // Resident CTAs per SM the register allocation must allow.
 template <int KMAX, int NT>
 constexpr int min_ctas() {
-    return NT < 128 ? 1 : (KMAX <= 4 ? 3 : 1);
+    return NT < 128 ? 1 : (KMAX <= 3 ? 5 : (KMAX == 4 ? 3 : 1));
 }
 
 template <int K, int KMAX, int NT>
@@ -588,7 +649,12 @@ pass_kernel(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, 
                 if constexpr (KMAX >= 4 && K >= 4) { if (kk == 4) dense_op<4, K, NT>(tile, op, blob); }
                 if constexpr (KMAX >= 5 && K >= 5) { if (kk == 5) dense5_op<K, NT>(tile, op, blob); }
             } else if (op.kind == QSV_OP_RBLOCK) {
-                if constexpr (K >= 4) rblock_op<K, NT>(tile, op, blob);
+                if constexpr (K >= 3) {
+                    if (op.k == 3) rblock_op<K, NT, 3>(tile, op, blob);
+                }
+                if constexpr (K >= 4 && KMAX >= 4) {
+                    if (op.k == 4) rblock_op<K, NT, 4>(tile, op, blob);
+                }
             } else if (op.kind == QSV_OP_PHASEPROD) {
                 phaseprod_op<K, NT>(tile, op, blob, full_base);
             } else if (op.kind == QSV_OP_DIAG) {

@@ -508,11 +508,12 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                 flops += 8.0 * D * amps * frac;
             }
         } else if (od.kind == QSV_OP_RBLOCK) {
-            QSV_REQUIRE(od.k == 4, "op: RBLOCK needs exactly 4 block qubits");
+            QSV_REQUIRE(od.k == 3 || od.k == 4, "op: RBLOCK needs 3 or 4 block qubits");
             QSV_REQUIRE(od.prim_begin >= 0 && od.nprim >= 1 && od.prim_begin + od.nprim <= nprims,
                         "op: RBLOCK primitive range outside the primitive array");
-            QSV_REQUIRE(K >= 4, "op: RBLOCK needs a tile of >= 4 qubits");
-            for (int i = 0; i < 4; ++i) {
+            QSV_REQUIRE(K >= od.k, "op: RBLOCK wider than the tile");
+            const int KB = od.k;
+            for (int i = 0; i < KB; ++i) {
                 const int q = od.qubits[i];
                 QSV_REQUIRE(q < n_local && tpos_of[q] >= 0,
                             "op: RBLOCK qubit " + std::to_string(q) + " is not in the pass tile");
@@ -529,24 +530,35 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                 double fl = 0;
                 switch (pd.kind) {
                 case QSV_PRIM_U1:
-                    QSV_REQUIRE(pd.a >= 0 && pd.a < 4, "prim: U1 qubit index outside 0..3");
+                case QSV_PRIM_U1R:
+                case QSV_PRIM_U1I:
+                    QSV_REQUIRE(pd.a >= 0 && pd.a < KB, "prim: U1 qubit index outside the block");
                     dp.b = 0;
                     ne = 4;
-                    fl = 16;
+                    fl = pd.kind == QSV_PRIM_U1 ? 16 : 8;
+                    if (pd.kind != QSV_PRIM_U1) {
+                        QSV_REQUIRE(pd.mat_off >= 0 && static_cast<size_t>(pd.mat_off) + 4 <= pool_len,
+                                    "prim: matrix outside the pool");
+                        const double* m = pool + 2 * pd.mat_off;
+                        const bool ok = pd.kind == QSV_PRIM_U1R
+                                            ? (m[1] == 0 && m[3] == 0 && m[5] == 0 && m[7] == 0)
+                                            : (m[1] == 0 && m[2] == 0 && m[4] == 0 && m[7] == 0);
+                        QSV_REQUIRE(ok, "prim: U1R needs a real matrix, U1I real diagonal / imaginary off-diagonal");
+                    }
                     break;
                 case QSV_PRIM_U2:
-                    QSV_REQUIRE(pd.a >= 0 && pd.b > pd.a && pd.b < 4, "prim: U2 needs 0 <= a < b < 4");
+                    QSV_REQUIRE(pd.a >= 0 && pd.b > pd.a && pd.b < KB, "prim: U2 needs 0 <= a < b < k");
                     ne = 16;
                     fl = 32;
                     break;
                 case QSV_PRIM_CX:
-                    QSV_REQUIRE(pd.a >= 0 && pd.a < 4 && pd.b >= 0 && pd.b < 4 && pd.a != pd.b,
+                    QSV_REQUIRE(pd.a >= 0 && pd.a < KB && pd.b >= 0 && pd.b < KB && pd.a != pd.b,
                                 "prim: CX needs distinct block qubits");
                     break;
                 case QSV_PRIM_DIAG16:
                     dp.a = 3;  // routes to the default (diagonal) case of the switch
                     dp.b = 3;
-                    ne = 16;
+                    ne = 1 << KB;
                     fl = 6;
                     break;
                 default:
@@ -557,9 +569,9 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                     QSV_REQUIRE(pd.mat_off >= 0 && static_cast<size_t>(pd.mat_off) + ne <= pool_len,
                                 "prim: matrix outside the pool");
                     const double* m = pool + 2 * pd.mat_off;
-                    if (pd.kind == QSV_PRIM_U1 || pd.kind == QSV_PRIM_U2) {
+                    if (pd.kind != QSV_PRIM_DIAG16) {
                         // rotation variants: M_s[i][j] = M[i ^ s][j ^ s]
-                        const int dim = pd.kind == QSV_PRIM_U1 ? 2 : 4;
+                        const int dim = pd.kind == QSV_PRIM_U2 ? 4 : 2;
                         for (int sv = 0; sv < dim; ++sv)
                             for (int i = 0; i < dim; ++i)
                                 for (int j = 0; j < dim; ++j) {
@@ -575,7 +587,7 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                 flops += fl * amps * frac;
             }
             t.nprim = od.nprim;
-            step.geom.kmax = std::max(step.geom.kmax, 1);
+            step.geom.kmax = std::max(step.geom.kmax, KB == 4 ? 4 : 1);
         } else if (od.kind == QSV_OP_PHASEPROD) {
             QSV_REQUIRE(od.k == 0, "op: PHASEPROD takes its qubits as FACTOR primitives (k = 0)");
             QSV_REQUIRE(od.prim_begin >= 0 && od.nprim >= 0 && od.prim_begin + od.nprim <= nprims,
@@ -669,7 +681,7 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
             // only in the next bits would hit the same banks, so their member
             // order is rotated by XOR over the block slots sitting in bits 0..2.
             std::vector<int> lowslots;
-            for (int sl = 0; sl < 4; ++sl)
+            for (int sl = 0; sl < od.k; ++sl)
                 if (t.tpos[sl] < 3)
                     lowslots.push_back(sl);
             int a = 0;

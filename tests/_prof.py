@@ -8,6 +8,6 @@ e.set_basis(0)
 prof = e.profile()
 st = e.steps()
 for i, (p, s) in enumerate(zip(prof, st)):
-    if i < 12:
+    if i < 200:
         print(i, "%.3f ms" % p, s["nops"], "%.1f GB/s" % (s["hbm_bytes"] / p / 1e6))
 print("total", sum(prof))

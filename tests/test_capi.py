@@ -66,9 +66,9 @@ def test_program_validate_rejects_bad_programs():
     op.qubits[0] = 12
     st = Step(kind=0, tile_k=10, nhigh=1, op_begin=0, op_count=1)
     st.high[0] = 12
-    assert L.qsv_program_validate(16, 16, 0, C.byref(st), 1, C.byref(op), 1, None, 0, pool, 4) == 0
+    assert L.qsv_program_validate(16, 16, 0, C.byref(st), 1, C.byref(op), 1, None, 0, pool, C.c_size_t(4)) == 0
     st.nhigh = 0  # target 12 no longer inside the tile
-    assert L.qsv_program_validate(16, 16, 0, C.byref(st), 1, C.byref(op), 1, None, 0, pool, 4) == -1
+    assert L.qsv_program_validate(16, 16, 0, C.byref(st), 1, C.byref(op), 1, None, 0, pool, C.c_size_t(4)) == -1
     st.nhigh = 1
     op.mat_off = 3  # matrix outside the pool
-    assert L.qsv_program_validate(16, 16, 0, C.byref(st), 1, C.byref(op), 1, None, 0, pool, 4) == -1
+    assert L.qsv_program_validate(16, 16, 0, C.byref(st), 1, C.byref(op), 1, None, 0, pool, C.c_size_t(4)) == -1

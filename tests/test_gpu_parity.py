@@ -39,6 +39,8 @@ OPTS = {
     "dense5": pkg.PlanOptions(register_blocks=False, fuse_k=5, pass_budget=500),
     "unfused": pkg.PlanOptions(fusion=False, multi_op_passes=False),
     "tile8": pkg.PlanOptions(tile_k=8, pass_budget=200),
+    "rblock4": pkg.PlanOptions(rblock_k=4, tile_k=11),
+    "tile11": pkg.PlanOptions(tile_k=11),
 }
 
 
