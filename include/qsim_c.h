@@ -102,6 +102,39 @@ int qsim_engine_step_info(qsim_engine* e, int i, int* kind, int* nops, double* h
                           double* nvl_bytes);
 int qsim_engine_profile(qsim_engine* e, float* ms_per_step);
 
+/* ---- SPEC-level passes (reference semantics) ---- */
+typedef struct qsim_fusion_stats {
+    int64_t gates_before, gates_after, merges_same_qubit, merges_cu, merges_kronecker, passes;
+    double compression_ratio, cost_before, cost_after;
+} qsim_fusion_stats;
+
+typedef struct qsim_dist_report {
+    int32_t ranks, reserved;
+    int64_t swaps;
+    double seconds;
+    int64_t peak_bytes[64];
+} qsim_dist_report;
+
+/* build_dag: writes up to cap (i, j) edge pairs; returns the edge count (< 0: error). */
+int64_t qsim_dag_edges(const qsim_circuit* c, int32_t* pairs, int64_t cap);
+/* gate_cost of gate i for an n-qubit state. */
+int qsim_gate_cost(const qsim_circuit* c, int64_t i, int n, double* out);
+/* contract(c, cap) -> FUSED circuit + stats. */
+int qsim_contract(const qsim_circuit* c, int cap, qsim_circuit** out, qsim_fusion_stats* stats);
+/* plan_groups: group_of[i] = group id of gate i or -1 (residual); returns #groups. */
+int qsim_plan_groups(const qsim_circuit* c, int S, int local_qubits, int32_t* group_of);
+/* stagger_schedule(G, S): table[g*S + tau]. */
+int qsim_stagger_schedule(int G, int S, int32_t* table);
+/* execute_staggered on host amplitudes for the gates whose group id == group. */
+int qsim_execute_staggered(const qsim_circuit* c, int S, int local_qubits, int group, double* amps);
+/* classify_gate (0 LOCAL, 1 TARGET_REMOTE, 2 CONTROL_REMOTE, 3 BOTH_REMOTE). */
+int qsim_classify_gate(const qsim_circuit* c, int64_t i, int m, int* out);
+int qsim_peer_rank(int r, int t, int l, int* out);
+/* run_distributed over 2^m GPUs (devices[r], NULL = 0..2^m-1) from |0...0>;
+ * gathers all 2^n amplitudes into amps (host). */
+int qsim_run_distributed(const qsim_circuit* c, int m, int b, int buffers, const int* devices,
+                         const qsim_plan_opts* opts, double* amps, qsim_dist_report* report);
+
 /* ---- memtrack (ref memtrack.hpp:12-26) scripted session, for parity tests ----
  * ops[2*i] = kind (0 enable, 1 register_thread, 2 set_phase, 3 on_alloc,
  * 4 on_free, 5 reset, 6 disable), ops[2*i+1] = argument; writes

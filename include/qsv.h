@@ -69,6 +69,9 @@ int qsv_ctx_create(int device, int rank, int nranks, const void* comm_id, qsv_ct
 int qsv_ctx_destroy(qsv_ctx* ctx);
 /* The cudaStream_t (as void*) all work of this context is ordered on. */
 void* qsv_ctx_stream(qsv_ctx* ctx);
+/* Bytes of swap staging buffers currently held by the context (BBOP memory
+ * accounting: per rank <= (2^l + B*2^b)*16 B + overhead). */
+int qsv_ctx_staging_bytes(qsv_ctx* ctx, size_t* out);
 /* Blocks until all work queued on the context has finished. */
 int qsv_sync(qsv_ctx* ctx);
 /* Thread-local description of the last failure on this thread. */

@@ -1,7 +1,12 @@
 // Definitions for include/qsim_c.h: exception-free C facade over qsim.
 #include "qsim_c.h"
 
+#include "qsim/dag.hpp"
 #include "qsim/device.hpp"
+#include "qsim/exchange.hpp"
+#include "qsim/fusion.hpp"
+#include "qsim/partition.hpp"
+#include "qsim/stagger.hpp"
 #include "qsim/generators.hpp"
 #include "qsim/memtrack.hpp"
 #include "qsim/planner.hpp"
@@ -386,6 +391,134 @@ int qsim_engine_profile(qsim_engine* e, float* ms) {
     return guard([&] {
         REQUIRE(e && ms, "qsim_engine_profile: null argument");
         qsim::qsv_check(qsv_program_profile(e->st->get(), e->eng->program(), ms), "qsv_program_profile");
+        return QSV_OK;
+    });
+}
+
+int64_t qsim_dag_edges(const qsim_circuit* c, int32_t* pairs, int64_t cap) {
+    if (!c) {
+        t_err = "qsim_dag_edges: null circuit";
+        return QSV_E_ARG;
+    }
+    int64_t n = 0;
+    const int rc = guard([&] {
+        const qsim::DepGraph g = qsim::build_dag(c->c);
+        for (const auto& e : g.edges()) {
+            if (pairs && n < cap) {
+                pairs[2 * n] = e.first;
+                pairs[2 * n + 1] = e.second;
+            }
+            ++n;
+        }
+        return QSV_OK;
+    });
+    return rc == QSV_OK ? n : rc;
+}
+
+int qsim_gate_cost(const qsim_circuit* c, int64_t i, int n, double* out) {
+    return guard([&] {
+        REQUIRE(c && out && i >= 0 && i < static_cast<int64_t>(c->c.gates.size()), "qsim_gate_cost: bad argument");
+        *out = qsim::gate_cost(c->c.gates[i], n);
+        return QSV_OK;
+    });
+}
+
+int qsim_contract(const qsim_circuit* c, int cap, qsim_circuit** out, qsim_fusion_stats* stats) {
+    return guard([&] {
+        REQUIRE(c && out, "qsim_contract: null argument");
+        auto [res, plan, st] = qsim::contract(c->c, cap);
+        (void)plan;
+        if (stats) {
+            stats->gates_before = static_cast<int64_t>(st.gates_before);
+            stats->gates_after = static_cast<int64_t>(st.gates_after);
+            stats->merges_same_qubit = static_cast<int64_t>(st.merges_same_qubit);
+            stats->merges_cu = static_cast<int64_t>(st.merges_cu);
+            stats->merges_kronecker = static_cast<int64_t>(st.merges_kronecker);
+            stats->passes = static_cast<int64_t>(st.passes);
+            stats->compression_ratio = st.compression_ratio;
+            stats->cost_before = st.cost_before;
+            stats->cost_after = st.cost_after;
+        }
+        *out = new qsim_circuit{std::move(res)};
+        return QSV_OK;
+    });
+}
+
+int qsim_plan_groups(const qsim_circuit* c, int S, int local_qubits, int32_t* group_of) {
+    int ng = 0;
+    const int rc = guard([&] {
+        REQUIRE(c && group_of, "qsim_plan_groups: null argument");
+        auto [groups, residual] = qsim::plan_groups(c->c, qsim::build_dag(c->c), S, local_qubits);
+        for (std::size_t i = 0; i < c->c.gates.size(); ++i)
+            group_of[i] = -1;
+        for (std::size_t g = 0; g < groups.size(); ++g)
+            for (int gi : groups[g].gates)
+                group_of[gi] = static_cast<int32_t>(g);
+        ng = static_cast<int>(groups.size());
+        return QSV_OK;
+    });
+    return rc == QSV_OK ? ng : rc;
+}
+
+int qsim_stagger_schedule(int G, int S, int32_t* table) {
+    return guard([&] {
+        REQUIRE(table, "qsim_stagger_schedule: null table");
+        const auto t = qsim::stagger_schedule(G, S);
+        for (int g = 0; g < G; ++g)
+            for (int tau = 0; tau < S; ++tau)
+                table[g * S + tau] = t[g][tau];
+        return QSV_OK;
+    });
+}
+
+int qsim_execute_staggered(const qsim_circuit* c, int S, int local_qubits, int group, double* amps) {
+    return guard([&] {
+        REQUIRE(c && amps, "qsim_execute_staggered: null argument");
+        auto [groups, residual] = qsim::plan_groups(c->c, qsim::build_dag(c->c), S, local_qubits);
+        REQUIRE(group >= 0 && group < static_cast<int>(groups.size()), "qsim_execute_staggered: no such group");
+        qsim::StateVector sv(c->c.n);
+        std::memcpy(static_cast<void*>(sv.data()), amps, sizeof(qsim::Amp) * sv.size());
+        qsim::execute_staggered(sv, c->c, groups[group], 1);
+        std::memcpy(amps, sv.data(), sizeof(qsim::Amp) * sv.size());
+        return QSV_OK;
+    });
+}
+
+int qsim_classify_gate(const qsim_circuit* c, int64_t i, int m, int* out) {
+    return guard([&] {
+        REQUIRE(c && out && i >= 0 && i < static_cast<int64_t>(c->c.gates.size()), "qsim_classify_gate: bad argument");
+        const qsim::PartitionPlan p(c->c.n, m, 0, 2);
+        *out = static_cast<int>(qsim::classify_gate(c->c.gates[i], p));
+        return QSV_OK;
+    });
+}
+
+int qsim_peer_rank(int r, int t, int l, int* out) {
+    return guard([&] {
+        REQUIRE(out, "qsim_peer_rank: null output");
+        *out = qsim::peer_rank(r, t, l);
+        return QSV_OK;
+    });
+}
+
+int qsim_run_distributed(const qsim_circuit* c, int m, int b, int buffers, const int* devices,
+                         const qsim_plan_opts* opts, double* amps, qsim_dist_report* report) {
+    return guard([&] {
+        REQUIRE(c && amps, "qsim_run_distributed: null argument");
+        const qsim::PartitionPlan p(c->c.n, m, b, buffers);
+        std::vector<int> dev;
+        if (devices)
+            dev.assign(devices, devices + p.ranks());
+        qsim::DistributedReport rep;
+        qsim::StateVector sv = qsim::run_distributed(c->c, p, dev, &rep, to_opts(opts));
+        std::memcpy(amps, sv.data(), sizeof(qsim::Amp) * sv.size());
+        if (report) {
+            report->ranks = rep.ranks;
+            report->swaps = static_cast<int64_t>(rep.swaps);
+            report->seconds = rep.seconds;
+            for (std::size_t r = 0; r < rep.peak_bytes.size() && r < 64; ++r)
+                report->peak_bytes[r] = static_cast<int64_t>(rep.peak_bytes[r]);
+        }
         return QSV_OK;
     });
 }

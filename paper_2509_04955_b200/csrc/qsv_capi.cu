@@ -302,6 +302,12 @@ extern "C" int qsv_ctx_destroy(qsv_ctx* ctx) {
     return QSV_OK;
 }
 
+extern "C" int qsv_ctx_staging_bytes(qsv_ctx* ctx, size_t* out) {
+    QSV_REQUIRE(ctx != nullptr && out != nullptr, "qsv_ctx_staging_bytes: null argument");
+    *out = ctx->stage_bytes;
+    return QSV_OK;
+}
+
 extern "C" void* qsv_ctx_stream(qsv_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 extern "C" int qsv_sync(qsv_ctx* ctx) {
