@@ -77,6 +77,10 @@ int qsim_circuit_fused(const qsim_circuit* c, const qsim_plan_opts* opts, qsim_c
 int qsim_circuit_plan(const qsim_circuit* c, const qsim_plan_opts* opts, int n_local, int rank,
                       qsim_plan_stats* stats);
 void qsim_circuit_free(qsim_circuit* c);
+/* Exports the device program of the plan (include/qsv.h structures).  Call
+ * with NULL arrays to get the counts, then again with buffers of that size. */
+int qsim_plan_export(const qsim_circuit* c, const qsim_plan_opts* opts, int n_local, int* nsteps, int* nops,
+                     int* nprims, int64_t* pool_len, void* steps, void* ops, void* prims, double* pool);
 
 /* ---- engine: one rank's GPU, a planned circuit and its device state ---- */
 int qsim_engine_create(const qsim_circuit* c, const qsim_plan_opts* opts, int device, int rank,

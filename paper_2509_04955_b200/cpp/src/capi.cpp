@@ -258,6 +258,29 @@ int qsim_circuit_plan(const qsim_circuit* c, const qsim_plan_opts* opts, int n_l
 
 void qsim_circuit_free(qsim_circuit* c) { delete c; }
 
+int qsim_plan_export(const qsim_circuit* c, const qsim_plan_opts* opts, int n_local, int* nsteps, int* nops,
+                     int* nprims, int64_t* pool_len, void* steps, void* ops, void* prims, double* pool) {
+    return guard([&] {
+        REQUIRE(c && nsteps && nops && nprims && pool_len, "qsim_plan_export: null argument");
+        qsim::PlanOptions o = to_opts(opts);
+        o.n_local = n_local;
+        const qsim::Plan p = qsim::make_plan(c->c, o);
+        *nsteps = static_cast<int>(p.steps.size());
+        *nops = static_cast<int>(p.ops.size());
+        *nprims = static_cast<int>(p.prims.size());
+        *pool_len = static_cast<int64_t>(p.pool.size() / 2);
+        if (steps)
+            std::memcpy(steps, p.steps.data(), p.steps.size() * sizeof(qsv_step_desc));
+        if (ops)
+            std::memcpy(ops, p.ops.data(), p.ops.size() * sizeof(qsv_op_desc));
+        if (prims)
+            std::memcpy(prims, p.prims.data(), p.prims.size() * sizeof(qsv_prim_desc));
+        if (pool)
+            std::memcpy(pool, p.pool.data(), p.pool.size() * sizeof(double));
+        return QSV_OK;
+    });
+}
+
 int qsim_engine_create(const qsim_circuit* c, const qsim_plan_opts* opts, int device, int rank, int nranks,
                        const void* comm_id, qsim_engine** out) {
     return guard([&] {
