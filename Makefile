@@ -14,19 +14,25 @@ CU_SRC   := $(wildcard $(PKG)/csrc/*.cu)
 CU_OBJ   := $(patsubst $(PKG)/csrc/%.cu,build/cu/%.o,$(CU_SRC))
 CPP_SRC  := $(wildcard $(PKG)/cpp/src/*.cpp)
 CPP_OBJ  := $(patsubst $(PKG)/cpp/src/%.cpp,build/cpp/%.o,$(CPP_SRC))
-HDRS     := $(wildcard include/*.h) $(wildcard $(PKG)/csrc/*.h) $(wildcard $(PKG)/cpp/include/qsim/*.hpp)
+HDRS     := $(wildcard include/*.h) $(wildcard $(PKG)/csrc/*.h) $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/cpp/include/qsim/*.hpp)
 TESTS_CPP:= $(wildcard tests/cpp/*.cpp)
 TEST_BIN := $(patsubst tests/cpp/%.cpp,build/tests/%,$(TESTS_CPP))
 
 all: $(LIB)/libqsv.so $(LIB)/libqsim.so oracle/liboracle.so ref tests-cpp
 
-build/cu/%.o: $(PKG)/csrc/%.cu $(HDRS)
+build/cu/%.o: $(PKG)/csrc/%.cu $(HDRS) build/jit_src.inc
 	@mkdir -p $(dir $@)
-	$(NVCC) $(NVFLAGS) -c $< -o $@
+	$(NVCC) $(NVFLAGS) -Ibuild -c $< -o $@
+
+# device source embedded in libqsv.so for NVRTC (jit.cu)
+build/jit_src.inc: $(PKG)/csrc/device_types.h $(PKG)/csrc/pass_device.cuh
+	@mkdir -p build
+	{ printf 'R"QSVJIT('; grep -v '^#pragma once' $(PKG)/csrc/device_types.h; \
+	  grep -v -e '^#pragma once' -e '#include "device_types.h"' $(PKG)/csrc/pass_device.cuh; printf ')QSVJIT"'; } > $@
 
 $(LIB)/libqsv.so: $(CU_OBJ)
 	@mkdir -p $(LIB)
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lnccl -ldl
 
 build/cpp/%.o: $(PKG)/cpp/src/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)

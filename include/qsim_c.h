@@ -45,7 +45,7 @@ typedef struct qsim_plan_opts {
     int32_t register_blocks;  /* group native gates on <= 4 qubits (RBLOCK)     */
     double pass_budget;       /* DP cost units per amplitude per pass           */
     int32_t rblock_k;         /* register-block width: 3 or 4 qubits            */
-    int32_t reserved;
+    int32_t jit;              /* NVRTC-specialised pass kernels (1) or the interpreter (0) */
 } qsim_plan_opts;
 
 typedef struct qsim_plan_stats {
@@ -105,6 +105,8 @@ int qsim_engine_nsteps(qsim_engine* e);
 int qsim_engine_step_info(qsim_engine* e, int i, int* kind, int* nops, double* hbm_bytes, double* flops,
                           double* nvl_bytes);
 int qsim_engine_profile(qsim_engine* e, float* ms_per_step);
+/* JIT statistics: distinct specialised kernels and compile seconds (0 = cache hits). */
+int qsim_engine_jit_info(qsim_engine* e, int* kernels, double* seconds);
 
 /* ---- SPEC-level passes (reference semantics) ---- */
 typedef struct qsim_fusion_stats {

@@ -177,6 +177,14 @@ int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local,
                        const qsv_prim_desc* prims, int nprims,
                        const double* pool, size_t pool_len, qsv_program** out);
 int qsv_program_free(qsv_program* prog);
+/* Specialises the program's passes: each distinct pass structure is emitted
+ * as straight-line CUDA (constants for the tile enumeration, slot positions and
+ * primitive sequence) and compiled by NVRTC for sm_100a; at most max_kernels
+ * distinct kernels (other passes keep the interpreter kernel).  Synchronous;
+ * *seconds receives the compile time (0 for disk-cache hits).  Returns
+ * QSV_E_STATE when NVRTC is unavailable (the program stays valid). */
+int qsv_program_jit(qsv_program* prog, int max_kernels, double* seconds);
+int qsv_program_jit_info(qsv_program* prog, int* kernels, int* steps_jitted);
 /* Host-only dry run of qsv_program_create's validation and tile compilation
  * (no device needed): returns QSV_OK iff the program would be accepted for
  * rank `rank`.  Used by CPU tests of the planner. */

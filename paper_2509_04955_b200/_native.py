@@ -55,7 +55,7 @@ class qsim_plan_opts(C.Structure):
         ("register_blocks", C.c_int32),
         ("pass_budget", C.c_double),
         ("rblock_k", C.c_int32),
-        ("reserved", C.c_int32),
+        ("jit", C.c_int32),
     ]
 
 
@@ -141,18 +141,20 @@ class PlanOptions:
     pass_budget: float = 72.0
     register_blocks: bool = True
     rblock_k: int = 4
+    jit: bool = True
 
     @classmethod
     def default(cls) -> "PlanOptions":
         o = qsim_plan_opts()
         load_qsim().qsim_default_opts(C.byref(o))
         return cls(o.tile_k, o.min_low, o.fuse_k, bool(o.fusion), bool(o.multi_op_passes),
-                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k)
+                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k, bool(o.jit))
 
     def to_c(self) -> qsim_plan_opts:
         return qsim_plan_opts(self.tile_k, self.min_low, self.fuse_k, int(self.fusion),
                               int(self.multi_op_passes), self.chunk_log2, self.nbuf,
-                              int(self.register_blocks), float(self.pass_budget), int(self.rblock_k), 0)
+                              int(self.register_blocks), float(self.pass_budget), int(self.rblock_k),
+                              int(self.jit))
 
 
 class Circuit:
@@ -327,6 +329,11 @@ class Engine:
             out.append({"kind": "pass" if kind.value == 0 else "swap", "nops": nops.value,
                         "hbm_bytes": hbm.value, "flops": fl.value, "nvl_bytes": nvl.value})
         return out
+
+    def jit_info(self) -> dict:
+        k, s = C.c_int(), C.c_double()
+        _check(load_qsim().qsim_engine_jit_info(self._h, C.byref(k), C.byref(s)), "jit_info")
+        return {"kernels": k.value, "seconds": s.value}
 
     def profile(self) -> list[float]:
         n = load_qsim().qsim_engine_nsteps(self._h)

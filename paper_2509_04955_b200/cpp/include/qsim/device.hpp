@@ -70,6 +70,8 @@ class Engine {
     Engine& operator=(const Engine&) = delete;
 
     const Plan& plan() const { return plan_; }
+    double jit_seconds() const { return jit_seconds_; }
+    int jit_kernels() const { return jit_kernels_; }
     qsv_program* program() const { return prog_; }
     // Enqueues the whole circuit on the context stream (asynchronous).
     void run(DeviceState& st) const;
@@ -78,6 +80,8 @@ class Engine {
     DeviceContext& ctx_;
     Plan plan_;
     qsv_program* prog_ = nullptr;
+    double jit_seconds_ = 0.0;
+    int jit_kernels_ = 0;
 };
 
 } // namespace qsim

@@ -65,6 +65,8 @@ struct PlanOptions {
     int n_local = -1;         // local qubits per rank (-1: all, single GPU)
     int chunk_log2 = 22;      // BBOP batch: 2^b amplitudes per swap message
     int nbuf = 2;             // BBOP buffers B (default 2)
+    bool jit = true;          // NVRTC-specialised pass kernels (falls back to the interpreter kernel)
+    int jit_max_kernels = 512;  // distinct pass structures compiled at most
 };
 
 struct PlanStats {

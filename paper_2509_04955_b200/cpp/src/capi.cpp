@@ -62,6 +62,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.nbuf = o->nbuf;
     p.pass_budget = o->pass_budget;
     p.rblock_k = o->rblock_k;
+    p.jit = o->jit != 0;
     return p;
 }
 
@@ -114,6 +115,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->nbuf = p.nbuf;
     out->pass_budget = p.pass_budget;
     out->rblock_k = p.rblock_k;
+    out->jit = p.jit;
 }
 
 int qsim_circuit_generate(const char* spec, qsim_circuit** out) {
@@ -565,6 +567,15 @@ void qsim_memtrack_script(const long long* ops, int nops, int nranks, unsigned l
         for (int p = 0; p < 2; ++p)
             peaks[2 * r + p] = peak_bytes(r, static_cast<Phase>(p));
     unregister_thread();
+}
+
+int qsim_engine_jit_info(qsim_engine* e, int* kernels, double* seconds) {
+    return guard([&] {
+        REQUIRE(e, "qsim_engine_jit_info: null engine");
+        if (kernels) *kernels = e->eng->jit_kernels();
+        if (seconds) *seconds = e->eng->jit_seconds();
+        return QSV_OK;
+    });
 }
 
 int qsim_run_local_host(const qsim_circuit* c, const qsim_plan_opts* opts, double* amps) {

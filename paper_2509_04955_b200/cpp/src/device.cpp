@@ -3,6 +3,7 @@
 #include "qsim/kernels.hpp"
 #include "qsim/memtrack.hpp"
 
+#include <cstdio>
 #include <mutex>
 
 namespace qsim {
@@ -80,6 +81,20 @@ Engine::Engine(DeviceContext& ctx, const Circuit& c, const PlanOptions& opt) : c
                                  static_cast<int>(plan_.prims.size()), plan_.pool.data(),
                                  plan_.pool.size() / 2, &prog_),
               "qsv_program_create");
+    if (o.jit && o.jit_max_kernels > 0) {
+        const int rc = qsv_program_jit(prog_, o.jit_max_kernels, &jit_seconds_);
+        if (rc == QSV_OK) {
+            int steps = 0;
+            qsv_program_jit_info(prog_, &jit_kernels_, &steps);
+        } else {
+            static bool warned = false;
+            if (!warned) {
+                std::fprintf(stderr, "qsim: JIT unavailable, using the interpreter pass kernel (%s)\n",
+                             qsv_last_error());
+                warned = true;
+            }
+        }
+    }
 }
 
 Engine::~Engine() { qsv_program_free(prog_); }

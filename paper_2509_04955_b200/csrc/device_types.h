@@ -1,0 +1,92 @@
+// Device-visible data structures of a compiled pass, shared by the nvcc-built
+// interpreter kernel (pass_kernel.cu) and the NVRTC-specialised pass kernels
+// (jit.cu).  Must compile both as host C++ and under NVRTC (no host headers).
+#pragma once
+
+#if defined(__CUDACC_RTC__)
+typedef unsigned char uint8_t;
+typedef signed char int8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#else
+#include <cstdint>
+#endif
+
+#ifndef QSV_H
+// values mirror include/qsv.h (static_assert-checked in qsv_internal.h)
+#define QSV_MAX_DENSE_K 5
+#define QSV_MAX_DIAG_K 8
+#define QSV_MAX_HIGH 8
+#define QSV_OP_DENSE 0
+#define QSV_OP_DIAG 1
+#define QSV_OP_XPERM 2
+#define QSV_OP_RBLOCK 3
+#define QSV_OP_PHASEPROD 4
+#define QSV_PRIM_U1 0
+#define QSV_PRIM_U2 1
+#define QSV_PRIM_CX 2
+#define QSV_PRIM_DIAG16 3
+#define QSV_PRIM_FACTOR 4
+#define QSV_PRIM_U1R 5
+#define QSV_PRIM_U1I 6
+#endif
+
+namespace qsv {
+
+// One op compiled against the tile layout of its pass.  A pass is uploaded as
+// one "blob" = [TileOp x nops][member-offset tables][matrices / diagonal
+// tables]; each CTA copies the blob to shared memory once and every later read
+// is a warp-broadcast LDS.
+struct TileOp {
+    int32_t kind;       // QSV_OP_*
+    int32_t k;          // DENSE/XPERM: number of targets; DIAG: number of qubits; RBLOCK: slots
+    int32_t nfix;       // number of sorted positions in fixpos[]
+    uint32_t tctrl;     // tile-local control bits (must be 1)
+    uint64_t xctrl;     // full-index control bits outside the tile (CTA-uniform test)
+    uint32_t mat_byte;  // byte offset (in the blob) of the matrix / diagonal table
+    uint32_t off_byte;  // DENSE: byte offset of the 2^k member-offset table (uint32)
+    uint32_t tmask;     // DIAG: tile positions of the in-tile qubits (table bits 0..nin-1)
+    int32_t nin;        // DIAG: number of in-tile qubits
+    int8_t tpos[QSV_MAX_DIAG_K];  // DENSE/XPERM/RBLOCK: tile-local position of target/slot i
+    int8_t xbit[QSV_MAX_DIAG_K];  // DIAG: full-index bit of out-of-tile qubit j (table bit nin+j)
+    int8_t fixpos[24];            // ascending tile positions fixed during group enumeration
+    uint32_t fmask;               // OR of 1 << fixpos[i]
+    uint32_t ptab_byte;           // DIAG: byte offset of pext tables (uint8 [32] low, [64] high)
+    uint32_t prim_byte;           // RBLOCK: DevPrim list; PHASEPROD: ExtFactor list
+    int32_t nprim;
+    uint32_t rot_tab;             // RBLOCK: 4-bit member rotation per lane & 7 (bank spreading)
+    uint32_t pad2[3];
+};
+static_assert(sizeof(TileOp) % 16 == 0, "TileOp must keep 16-B alignment in the blob");
+
+// RBLOCK primitive as stored in the blob.
+struct DevPrim {
+    uint8_t kind;       // QSV_PRIM_U1 / U1R / U1I / U2 / CX / DIAG16
+    uint8_t a, b;       // block-local qubit indices (0..3)
+    uint8_t pad;
+    uint32_t data_byte; // blob offset of the matrix / table; 2x2 kinds store 2 variants
+                        // (U, XUX), U2 stores 4 (conjugated by X on a, b), one per
+                        // member rotation of the lane
+};
+
+// PHASEPROD factor on a qubit outside the tile (CTA-uniform).
+struct ExtFactor {
+    double re, im;
+    int32_t bit;        // full-index bit
+    int32_t pad[3];
+};
+
+// Tile geometry of a pass as passed to the kernels.
+struct GeomArg {
+    int32_t L, nhigh;
+    int32_t high[QSV_MAX_HIGH];
+};
+
+// Largest per-pass blob (bytes of shared memory on top of the tile buffers).
+constexpr uint32_t kMaxBlobBytes = 40 * 1024;
+// Tile buffers per CTA (TMA double buffering).
+constexpr int kNumBuf = 2;
+
+} // namespace qsv

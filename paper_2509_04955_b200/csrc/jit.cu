@@ -1,0 +1,467 @@
+// NVRTC specialisation of pass kernels (host code).
+//
+// The interpreter kernel (pass_kernel.cu) walks the pass's op records and
+// switches over ~40 register-block primitive bodies at run time: ~25 % of its
+// instructions are dispatch, the ~200 KB of SASS per variant misses the
+// instruction cache (ncu: 11 % `no_inst` stalls) and every CX through a
+// rotated slot costs selects.  Here each pass is re-emitted as straight-line
+// CUDA source — tile enumeration masks, slot positions, member-rotation table,
+// primitive sequence and blob offsets as compile-time constants, matrices still
+// read from the SMEM blob — and compiled by NVRTC to sm_100a SASS.  Passes with
+// the same structure share one kernel.  Compilation runs in parallel threads
+// and the cubins are cached on disk (QSV_JIT_CACHE, default ~/.cache/qsv_jit).
+//
+// The driver API is reached through cudaGetDriverEntryPoint and NVRTC through
+// dlopen, so libqsv.so has no link-time dependency on libcuda or libnvrtc.
+#include "qsv_internal.h"
+
+#include <cuda.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <sys/stat.h>
+#include <thread>
+#include <vector>
+
+namespace qsv {
+
+namespace {
+
+const char* kDeviceSource =
+#include "jit_src.inc"
+    ;
+
+// ------------------------------------------------------------------ loaders
+struct Nvrtc {
+    bool ok = false;
+    std::string why;
+    decltype(&nvrtcCreateProgram) create = nullptr;
+    decltype(&nvrtcCompileProgram) compile = nullptr;
+    decltype(&nvrtcGetCUBINSize) cubin_size = nullptr;
+    decltype(&nvrtcGetCUBIN) cubin = nullptr;
+    decltype(&nvrtcGetProgramLogSize) log_size = nullptr;
+    decltype(&nvrtcGetProgramLog) log = nullptr;
+    decltype(&nvrtcDestroyProgram) destroy = nullptr;
+};
+
+const Nvrtc& nvrtc() {
+    static Nvrtc n;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* names[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12"};
+        void* h = nullptr;
+        for (const char* nm : names)
+            if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL)))
+                break;
+        if (!h) {
+            n.why = "libnvrtc.so.12 not found";
+            return;
+        }
+        n.create = reinterpret_cast<decltype(n.create)>(dlsym(h, "nvrtcCreateProgram"));
+        n.compile = reinterpret_cast<decltype(n.compile)>(dlsym(h, "nvrtcCompileProgram"));
+        n.cubin_size = reinterpret_cast<decltype(n.cubin_size)>(dlsym(h, "nvrtcGetCUBINSize"));
+        n.cubin = reinterpret_cast<decltype(n.cubin)>(dlsym(h, "nvrtcGetCUBIN"));
+        n.log_size = reinterpret_cast<decltype(n.log_size)>(dlsym(h, "nvrtcGetProgramLogSize"));
+        n.log = reinterpret_cast<decltype(n.log)>(dlsym(h, "nvrtcGetProgramLog"));
+        n.destroy = reinterpret_cast<decltype(n.destroy)>(dlsym(h, "nvrtcDestroyProgram"));
+        n.ok = n.create && n.compile && n.cubin_size && n.cubin && n.log_size && n.log && n.destroy;
+        if (!n.ok)
+            n.why = "libnvrtc is missing symbols";
+    });
+    return n;
+}
+
+struct Driver {
+    bool ok = false;
+    CUresult (*module_load)(CUmodule*, const void*) = nullptr;
+    CUresult (*get_function)(CUfunction*, CUmodule, const char*) = nullptr;
+    CUresult (*set_attr)(CUfunction, CUfunction_attribute, int) = nullptr;
+    CUresult (*occupancy)(int*, CUfunction, int, size_t) = nullptr;
+    CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                       CUstream, void**, void**) = nullptr;
+    CUresult (*unload)(CUmodule) = nullptr;
+};
+
+template <typename F>
+bool entry(const char* name, F& fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+        return false;
+    fn = reinterpret_cast<F>(p);
+    return true;
+}
+
+const Driver& driver() {
+    static Driver d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        d.ok = entry("cuModuleLoadData", d.module_load) && entry("cuModuleGetFunction", d.get_function) &&
+               entry("cuFuncSetAttribute", d.set_attr) &&
+               entry("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy) &&
+               entry("cuLaunchKernel", d.launch) && entry("cuModuleUnload", d.unload);
+    });
+    return d;
+}
+
+// ------------------------------------------------------------------ codegen
+int threads_for_k(int K) { return K >= 8 ? 128 : (K >= 6 ? 64 : 32); }
+
+std::string u32(uint32_t x) {
+    std::ostringstream o;
+    o << "0x" << std::hex << x << "u";
+    return o.str();
+}
+
+std::string u64(uint64_t x) {
+    std::ostringstream o;
+    o << "0x" << std::hex << x << "ull";
+    return o.str();
+}
+
+// Body of one pass (ops applied to one tile) as source text.
+std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
+    const int K = s.geom.K;
+    const int NT = threads_for_k(K);
+    const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
+    std::ostringstream o;
+    minb = 3;
+    for (int i = 0; i < s.nops; ++i) {
+        const TileOp& op = ops[i];
+        const std::string opref = "*reinterpret_cast<const qsv::TileOp*>(blob + " +
+                                  std::to_string(i * sizeof(TileOp)) + ")";
+        o << "  {\n";
+        if (op.xctrl)
+            o << "  if ((full_base & " << u64(op.xctrl) << ") == " << u64(op.xctrl) << ") {\n";
+        o << "  __syncthreads();\n";
+        switch (op.kind) {
+        case QSV_OP_DENSE:
+            if (op.k == 5) {
+                o << "  qsv::dense5_op<" << K << ", " << NT << ">(tile, " << opref << ", blob);\n";
+                minb = 1;
+            } else {
+                o << "  qsv::dense_op<" << op.k << ", " << K << ", " << NT << ">(tile, " << opref << ", blob);\n";
+            }
+            break;
+        case QSV_OP_DIAG:
+            o << "  qsv::diag_op<" << K << ", " << NT << ">(tile, " << opref << ", blob, full_base);\n";
+            break;
+        case QSV_OP_PHASEPROD:
+            o << "  qsv::phaseprod_op<" << K << ", " << NT << ">(tile, " << opref << ", blob, full_base);\n";
+            break;
+        case QSV_OP_XPERM:
+            o << "  qsv::xperm_op<" << K << ", " << NT << ">(tile, " << opref << ");\n";
+            break;
+        case QSV_OP_RBLOCK: {
+            const int KB = op.k;
+            const int NV = 1 << KB;
+            uint32_t m[4] = {0, 0, 0, 0};
+            for (int j = 0; j < KB; ++j)
+                m[j] = 1u << op.tpos[j];
+            uint32_t rot_any = 0;
+            for (int l = 0; l < 8; ++l)
+                rot_any |= (op.rot_tab >> (4 * l)) & 15u;
+            o << "  qsv::jit_rblock<" << K << ", " << NT << ", " << KB << ", " << u32(op.fmask) << ", "
+              << u32(op.tctrl) << ", " << u32(m[0]) << ", " << u32(m[1]) << ", " << u32(m[2]) << ", " << u32(m[3])
+              << ", " << u32(op.rot_tab) << ">(tile, [&](double2 (&v)[" << NV << "], uint32_t r) {\n";
+            o << "    (void)r;\n";
+            const DevPrim* pr = reinterpret_cast<const DevPrim*>(blob + op.prim_byte);
+            for (int p = 0; p < op.nprim; ++p) {
+                const DevPrim& q = pr[p];
+                const std::string mat = "reinterpret_cast<const double2*>(blob + " + std::to_string(q.data_byte) + ")";
+                const bool ra = (rot_any >> q.a) & 1u, rb = (rot_any >> q.b) & 1u;
+                switch (q.kind) {
+                case QSV_PRIM_U1:
+                case QSV_PRIM_U1R:
+                case QSV_PRIM_U1I: {
+                    const char* fn = q.kind == QSV_PRIM_U1 ? "rb_u1" : (q.kind == QSV_PRIM_U1R ? "rb_u1r" : "rb_u1i");
+                    o << "    qsv::" << fn << "<" << NV << ", " << int(q.a) << ">(v, " << mat;
+                    if (ra)
+                        o << " + 4u * ((r >> " << int(q.a) << ") & 1u)";
+                    o << ");\n";
+                    break;
+                }
+                case QSV_PRIM_U2:
+                    o << "    qsv::rb_u2<" << NV << ", " << int(q.a) << ", " << int(q.b) << ">(v, " << mat;
+                    if (ra || rb)
+                        o << " + 16u * (((r >> " << int(q.a) << ") & 1u) | (((r >> " << int(q.b) << ") & 1u) << 1))";
+                    o << ");\n";
+                    break;
+                case QSV_PRIM_CX:
+                    if (ra)
+                        o << "    qsv::rb_cx<" << NV << ", " << int(q.a) << ", " << int(q.b) << ">(v, r);\n";
+                    else
+                        o << "    qsv::rb_cx_plain<" << NV << ", " << int(q.a) << ", " << int(q.b) << ">(v);\n";
+                    break;
+                default:
+                    o << "    qsv::rb_diag<" << NV << ">(v, " << mat << ", " << (rot_any ? "r" : "0u") << ");\n";
+                    break;
+                }
+            }
+            o << "  });\n";
+            break;
+        }
+        default:
+            o << "  // unknown op kind\n";
+        }
+        if (op.xctrl)
+            o << "  }\n";
+        o << "  }\n";
+    }
+    return o.str();
+}
+
+std::string kernel_source(const std::string& name, int K, int minb, const std::string& body) {
+    std::ostringstream o;
+    const int NT = threads_for_k(K);
+    o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb << ") " << name
+      << "(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, uint32_t blob_bytes,\n"
+      << "    const __grid_constant__ qsv::GeomArg geom, uint64_t rank_base, uint64_t ntiles) {\n"
+      << "  qsv::pass_pipeline<" << K << ", " << NT << ">(psi, gblob, blob_bytes, geom, rank_base, ntiles,\n"
+      << "    [&](double2* tile, const unsigned char* blob, uint64_t full_base) {\n"
+      << "  (void)full_base;\n"
+      << body << "  });\n}\n";
+    return o.str();
+}
+
+uint64_t fnv1a(const std::string& s) {
+    uint64_t h = 1469598103934665603ull;
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+std::string cache_dir() {
+    if (const char* d = std::getenv("QSV_JIT_CACHE"))
+        return d;
+    const char* home = std::getenv("HOME");
+    return std::string(home ? home : "/tmp") + "/.cache/qsv_jit";
+}
+
+void mkdirs(const std::string& p) {
+    std::string cur;
+    std::stringstream ss(p);
+    std::string part;
+    if (!p.empty() && p[0] == '/')
+        cur = "/";
+    while (std::getline(ss, part, '/')) {
+        if (part.empty())
+            continue;
+        cur += part + "/";
+        mkdir(cur.c_str(), 0755);
+    }
+}
+
+// Compiles one translation unit to a cubin (or loads it from the cache).
+bool compile_unit(const std::string& src, std::vector<char>& cubin, std::string& err) {
+    static const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-diag-suppress=177,550"};
+    std::string key = src;
+    for (const char* op : opts)
+        key += op;
+    const std::string dir = cache_dir();
+    char hex[32];
+    std::snprintf(hex, sizeof(hex), "%016llx", static_cast<unsigned long long>(fnv1a(key)));
+    const std::string path = dir + "/qsv_" + hex + ".cubin";
+    {
+        std::ifstream in(path, std::ios::binary);
+        if (in) {
+            cubin.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
+            if (!cubin.empty())
+                return true;
+        }
+    }
+    const Nvrtc& n = nvrtc();
+    nvrtcProgram prog;
+    if (n.create(&prog, src.c_str(), "qsv_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+        err = "nvrtcCreateProgram failed";
+        return false;
+    }
+    const nvrtcResult rc = n.compile(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
+    if (rc != NVRTC_SUCCESS) {
+        size_t ls = 0;
+        n.log_size(prog, &ls);
+        std::string log(ls, '\0');
+        n.log(prog, log.data());
+        err = "NVRTC compile failed: " + log.substr(0, 2000);
+        n.destroy(&prog);
+        return false;
+    }
+    size_t cs = 0;
+    n.cubin_size(prog, &cs);
+    cubin.resize(cs);
+    n.cubin(prog, cubin.data());
+    n.destroy(&prog);
+    mkdirs(dir);
+    const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<uintptr_t>(&cubin));
+    {
+        std::ofstream out(tmp, std::ios::binary);
+        out.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
+    }
+    std::rename(tmp.c_str(), path.c_str());
+    return true;
+}
+
+} // namespace
+
+bool jit_available(std::string& why) {
+    if (!nvrtc().ok) {
+        why = nvrtc().why;
+        return false;
+    }
+    if (!driver().ok) {
+        why = "CUDA driver entry points unavailable";
+        return false;
+    }
+    return true;
+}
+
+int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::string why;
+    if (!jit_available(why)) {
+        set_error("qsv_program_jit: " + why);
+        return QSV_E_STATE;
+    }
+    // unique structures -> kernels
+    std::map<std::string, int> uniq;
+    std::vector<std::string> bodies;
+    std::vector<int> kernel_k, kernel_minb;
+    prog->jit_of_step.assign(prog->steps.size(), -1);
+    for (size_t i = 0; i < prog->steps.size(); ++i) {
+        const Step& s = prog->steps[i];
+        if (s.desc.kind != QSV_STEP_PASS || s.geom.K < 4)
+            continue;
+        int minb = 3;
+        const std::string body = gen_ops(s, prog->host_blobs.data() + s.blob_off, minb);
+        const std::string key = std::to_string(s.geom.K) + "|" + std::to_string(minb) + "|" + body;
+        auto it = uniq.find(key);
+        if (it == uniq.end()) {
+            if (static_cast<int>(bodies.size()) >= max_kernels)
+                continue;  // beyond the budget: this pass keeps the interpreter
+            it = uniq.emplace(key, static_cast<int>(bodies.size())).first;
+            bodies.push_back(body);
+            kernel_k.push_back(s.geom.K);
+            kernel_minb.push_back(minb);
+        }
+        prog->jit_of_step[i] = it->second;
+    }
+    const int nk = static_cast<int>(bodies.size());
+    if (nk == 0) {
+        if (seconds)
+            *seconds = 0;
+        return QSV_OK;
+    }
+    // translation units of up to 6 kernels, compiled concurrently
+    const int per_unit = 6;
+    const int nunits = (nk + per_unit - 1) / per_unit;
+    std::vector<std::string> srcs(nunits);
+    for (int u = 0; u < nunits; ++u) {
+        std::string src = kDeviceSource;
+        for (int k = u * per_unit; k < std::min(nk, (u + 1) * per_unit); ++k)
+            src += kernel_source("qsv_jit_" + std::to_string(k), kernel_k[k], kernel_minb[k], bodies[k]);
+        srcs[u] = std::move(src);
+    }
+    std::vector<std::vector<char>> cubins(nunits);
+    std::vector<std::string> errs(nunits);
+    std::vector<char> oks(nunits, 0);
+    const int nthreads = std::max(1, std::min(nunits, static_cast<int>(std::thread::hardware_concurrency())));
+    std::vector<std::thread> pool;
+    for (int w = 0; w < nthreads; ++w)
+        pool.emplace_back([&, w] {
+            for (int u = w; u < nunits; u += nthreads)
+                oks[u] = compile_unit(srcs[u], cubins[u], errs[u]) ? 1 : 0;
+        });
+    for (auto& t : pool)
+        t.join();
+    for (int u = 0; u < nunits; ++u)
+        if (!oks[u]) {
+            prog->jit_of_step.assign(prog->steps.size(), -1);
+            set_error("qsv_program_jit: " + errs[u]);
+            return QSV_E_CUDA;
+        }
+    // load modules and functions
+    const Driver& d = driver();
+    cudaSetDevice(prog->ctx->device);
+    cudaFree(nullptr);  // make sure the primary context is current
+    prog->jit_kernels.assign(nk, {});
+    for (int u = 0; u < nunits; ++u) {
+        CUmodule mod;
+        if (d.module_load(&mod, cubins[u].data()) != CUDA_SUCCESS) {
+            prog->jit_of_step.assign(prog->steps.size(), -1);
+            set_error("qsv_program_jit: cuModuleLoadData failed");
+            return QSV_E_CUDA;
+        }
+        prog->jit_modules.push_back(mod);
+        for (int k = u * per_unit; k < std::min(nk, (u + 1) * per_unit); ++k) {
+            CUfunction f;
+            const std::string name = "qsv_jit_" + std::to_string(k);
+            if (d.get_function(&f, mod, name.c_str()) != CUDA_SUCCESS) {
+                prog->jit_of_step.assign(prog->steps.size(), -1);
+                set_error("qsv_program_jit: cuModuleGetFunction failed for " + name);
+                return QSV_E_CUDA;
+            }
+            const int K = kernel_k[k];
+            const size_t tile_smem = sizeof(double2) * kNumBuf * (size_t{1} << K);
+            d.set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
+                       static_cast<int>(tile_smem + kMaxBlobBytes));
+            prog->jit_kernels[k].func = f;
+            prog->jit_kernels[k].nt = threads_for_k(K);
+            prog->jit_kernels[k].tile_smem = tile_smem;
+        }
+    }
+    for (auto& kv : prog->graphs)
+        cudaGraphExecDestroy(kv.second);
+    prog->graphs.clear();
+    if (seconds)
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return QSV_OK;
+}
+
+cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step, const unsigned char* d_blob,
+                       uint64_t rank_base, cudaStream_t stream) {
+    const Step& s = prog->steps[step];
+    const JitKernel& jk = prog->jit_kernels[prog->jit_of_step[step]];
+    const size_t smem = jk.tile_smem + s.blob_bytes;
+    int per_sm = 0;
+    const Driver& d = driver();
+    if (d.occupancy(&per_sm, static_cast<CUfunction>(jk.func), jk.nt, smem) != CUDA_SUCCESS || per_sm < 1)
+        per_sm = 1;
+    GeomArg ga{};
+    ga.L = s.geom.L;
+    ga.nhigh = s.geom.nhigh;
+    for (int i = 0; i < s.geom.nhigh; ++i)
+        ga.high[i] = s.geom.high[i];
+    const uint64_t tiles = st->size >> s.geom.K;
+    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * st->ctx->sm_count);
+    double2* psi = st->amps;
+    uint32_t bb = s.blob_bytes;
+    uint64_t rb = rank_base, nt = tiles;
+    void* args[] = {&psi, const_cast<unsigned char**>(&d_blob), &bb, &ga, &rb, &nt};
+    const CUresult r = d.launch(static_cast<CUfunction>(jk.func), static_cast<unsigned>(grid), 1, 1,
+                                static_cast<unsigned>(jk.nt), 1, 1, static_cast<unsigned>(smem),
+                                reinterpret_cast<CUstream>(stream), args, nullptr);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorLaunchFailure;
+}
+
+void jit_release(qsv_program* prog) {
+    if (prog->jit_modules.empty())
+        return;
+    const Driver& d = driver();
+    for (void* m : prog->jit_modules)
+        d.unload(static_cast<CUmodule>(m));
+    prog->jit_modules.clear();
+}
+
+} // namespace qsv

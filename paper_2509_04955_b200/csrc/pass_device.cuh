@@ -1,0 +1,673 @@
+// Device code of the fused multi-block pass (sm_100a), shared by the nvcc-built
+// interpreter kernel (pass_kernel.cu) and the NVRTC-specialised kernels (jit.cu).
+// See pass_kernel.cu for the design notes.  NVRTC-safe: no host headers.
+#pragma once
+
+#include "device_types.h"
+
+namespace qsv {
+
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(smem_src)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- arithmetic
+__device__ __forceinline__ void cmac(double2& acc, const double2 m, const double2 v) {
+    acc.x = fma(m.x, v.x, acc.x);
+    acc.x = fma(-m.y, v.y, acc.x);
+    acc.y = fma(m.x, v.y, acc.y);
+    acc.y = fma(m.y, v.x, acc.y);
+}
+
+__device__ __forceinline__ double2 cmul(const double2 a, const double2 b) {
+    double2 r;
+    r.x = fma(a.x, b.x, -a.y * b.y);
+    r.y = fma(a.x, b.y, a.y * b.x);
+    return r;
+}
+
+// Insert a zero bit at each of the ascending positions fixpos[0..nfix).
+__device__ __forceinline__ uint32_t deposit(uint32_t g, const int8_t* fixpos, int nfix) {
+    for (int i = 0; i < nfix; ++i) {
+        const uint32_t p = static_cast<uint32_t>(fixpos[i]);
+        const uint32_t lo = g & ((1u << p) - 1u);
+        g = ((g ^ lo) << 1) | lo;
+    }
+    return g;
+}
+
+// Groups of an op are enumerated directly in "deposited" form: with F the
+// mask of the op's fixed tile bits (targets + tile controls), the successor of
+// b = deposit(g) after a stride s is ((b | F) + deposit(s)) & ~F — the fixed
+// bits, forced to 1, carry the addition across themselves.  Three integer ops
+// per group instead of a loop over the fixed positions.
+__device__ __forceinline__ uint32_t next_group(uint32_t b, uint32_t F, uint32_t dstride) {
+    return ((b | F) + dstride) & ~F;
+}
+
+// ---------------------------------------------------------------- ops
+// Warp-level complex mat-vec for k <= 4 (D = 2^k <= 16).  LPG = D*S lanes
+// cooperate on one 2^k-amplitude group: lane (r, s) keeps columns
+// [s*D/S, (s+1)*D/S) of matrix row r in registers for the whole op, reads the
+// group members as SMEM broadcasts, and the S partial sums of a row are
+// combined with warp shuffles.  A warp processes 32/LPG groups per step, so
+// registers stay ~8*D/S per lane and no CTA barrier is needed inside the op
+// (only __syncwarp between the reads and the in-place writes of a group).
+template <int KK, int K, int NT>
+__device__ __forceinline__ void dense_op(double2* tile, const TileOp& op, const unsigned char* blob) {
+    constexpr int D = 1 << KK;
+    constexpr int S = D >= 8 ? 2 : 1;     // column splits
+    constexpr int LPG = D * S;            // lanes per group
+    constexpr int GPW = 32 / LPG;         // groups per warp step
+    constexpr int CPL = D / S;            // columns per lane
+    constexpr int NW = NT / 32;
+    constexpr uint32_t PER_STEP = NW * GPW;
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int sub = lane / LPG;
+    const int r = (lane % LPG) / S;
+    const int sp = (lane % LPG) % S;
+    const double2* M = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    const uint32_t* off = reinterpret_cast<const uint32_t*>(blob + op.off_byte);
+    double2 m[CPL];
+    uint32_t o[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+        m[c] = M[r * D + sp * CPL + c];
+        o[c] = off[sp * CPL + c];
+    }
+    const uint32_t my_off = off[r];
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    const uint32_t g = static_cast<uint32_t>(warp * GPW + sub);
+    uint32_t b = deposit(g, op.fixpos, nfix);
+    const uint32_t dstep = deposit(PER_STEP, op.fixpos, nfix);
+    const uint32_t steps = groups >= PER_STEP ? groups / PER_STEP : 1u;
+    const bool act = g < groups;
+#pragma unroll 1
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t idx = b | tctrl;
+        double2 acc = make_double2(0.0, 0.0);
+        if (act) {
+#pragma unroll
+            for (int c = 0; c < CPL; ++c)
+                cmac(acc, m[c], tile[idx | o[c]]);
+        }
+        if constexpr (S > 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+        }
+        __syncwarp();
+        if (act && sp == 0)
+            tile[idx | my_off] = acc;
+        b = next_group(b, F, dstep);
+    }
+}
+
+template <int K, int NT>
+__device__ __forceinline__ void xperm_op(double2* tile, const TileOp& op) {
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    const uint32_t tb = 1u << op.tpos[0];
+    if (threadIdx.x >= groups)
+        return;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+#pragma unroll 2
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t idx = b | tctrl;
+        const double2 a0 = tile[idx];
+        const double2 a1 = tile[idx | tb];
+        tile[idx] = a1;
+        tile[idx | tb] = a0;
+        b = next_group(b, F, dstep);
+    }
+}
+
+template <int K, int NT>
+__device__ __forceinline__ void diag_op(double2* tile, const TileOp& op, const unsigned char* blob,
+                                        uint64_t full_base) {
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    const int k = op.k;
+    const int nin = op.nin;
+    const double2* Dg = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    uint32_t e0 = 0;
+    for (int j = nin; j < k; ++j)
+        e0 |= static_cast<uint32_t>((full_base >> op.xbit[j - nin]) & 1ull) << j;
+    if (threadIdx.x >= groups)
+        return;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+    if (nin == 0) {
+        const double2 d = Dg[e0];
+#pragma unroll 4
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t idx = b | tctrl;
+            tile[idx] = cmul(d, tile[idx]);
+            b = next_group(b, F, dstep);
+        }
+    } else if (nin == 1) {
+        const int p = __ffs(op.tmask) - 1;
+        const double2 d0 = Dg[e0], d1 = Dg[e0 | 1u];
+#pragma unroll 4
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t idx = b | tctrl;
+            tile[idx] = cmul(((idx >> p) & 1u) ? d1 : d0, tile[idx]);
+            b = next_group(b, F, dstep);
+        }
+    } else {
+        const uint8_t* plo = blob + op.ptab_byte;
+        const uint8_t* phi = plo + 32;
+#pragma unroll 2
+        for (uint32_t st = 0; st < steps; ++st) {
+            const uint32_t idx = b | tctrl;
+            const uint32_t e = e0 | plo[idx & 31u] | phi[idx >> 5];
+            tile[idx] = cmul(Dg[e], tile[idx]);
+            b = next_group(b, F, dstep);
+        }
+    }
+}
+
+// k = 5 (D = 32): one thread per group, all 32 members in registers.
+template <int K, int NT>
+__device__ __forceinline__ void dense5_op(double2* tile, const TileOp& op, const unsigned char* blob) {
+    constexpr int D = 32;
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t groups = 1u << (K - nfix);
+    const double2* M = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    const uint32_t* off = reinterpret_cast<const uint32_t*>(blob + op.off_byte);
+    const bool many = groups >= static_cast<uint32_t>(NT);
+    const int R = many ? 1 : min(NT / static_cast<int>(groups), D);
+    const int rows = D / R;
+#pragma unroll 1
+    for (uint32_t base_t = 0; base_t < (many ? groups : 1u); base_t += NT) {
+        const int t = static_cast<int>(threadIdx.x);
+        const uint32_t g = many ? base_t + t : static_cast<uint32_t>(t) % groups;
+        const int rb = many ? 0 : t / static_cast<int>(groups);
+        const bool act = many ? g < groups : t < static_cast<int>(groups) * R;
+        double2 v[D];
+        uint32_t b = 0;
+        if (act) {
+            b = deposit(g, op.fixpos, nfix) | tctrl;
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                v[j] = tile[b | off[j]];
+        }
+        if (!many)
+            __syncthreads();
+        if (act) {
+#pragma unroll 1
+            for (int rr = 0; rr < rows; ++rr) {
+                const int row = rb * rows + rr;
+                double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < D; ++j)
+                    cmac(acc, M[row * D + j], v[j]);
+                tile[b | off[row]] = acc;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- RBLOCK
+// A register block holds one group of NV = 2^KB amplitudes (KB = 3 or 4 block
+// qubits) per thread and applies a list of native gates to it in registers;
+// the list is uniform over the CTA, so the per-primitive switch is a uniform
+// branch.  Register v[j] holds group member j ^ r, where r is this lane's
+// member rotation (it spreads the lanes of a quarter-warp over the SMEM
+// banks); the host stores every matrix in its rotated variants.
+template <int NV, int Q>
+__device__ __forceinline__ void rb_u1(double2 (&v)[NV], const double2* U) {
+    const double2 u00 = U[0], u01 = U[1], u10 = U[2], u11 = U[3];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (j & (1 << Q))
+            continue;
+        const double2 x0 = v[j], x1 = v[j | (1 << Q)];
+        double2 r0 = make_double2(0.0, 0.0), r1 = make_double2(0.0, 0.0);
+        cmac(r0, u00, x0);
+        cmac(r0, u01, x1);
+        cmac(r1, u10, x0);
+        cmac(r1, u11, x1);
+        v[j] = r0;
+        v[j | (1 << Q)] = r1;
+    }
+}
+
+// Real 2x2 (H, RY, products of them): the real and imaginary parts of the
+// amplitudes are transformed independently, 4 DFMA per amplitude.
+template <int NV, int Q>
+__device__ __forceinline__ void rb_u1r(double2 (&v)[NV], const double2* U) {
+    const double u00 = U[0].x, u01 = U[1].x, u10 = U[2].x, u11 = U[3].x;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (j & (1 << Q))
+            continue;
+        const double2 x0 = v[j], x1 = v[j | (1 << Q)];
+        v[j] = make_double2(fma(u00, x0.x, u01 * x1.x), fma(u00, x0.y, u01 * x1.y));
+        v[j | (1 << Q)] = make_double2(fma(u10, x0.x, u11 * x1.x), fma(u10, x0.y, u11 * x1.y));
+    }
+}
+
+// Real diagonal, imaginary off-diagonal 2x2 (RX): [[c0, i s01], [i s10, c1]].
+template <int NV, int Q>
+__device__ __forceinline__ void rb_u1i(double2 (&v)[NV], const double2* U) {
+    const double c0 = U[0].x, s01 = U[1].y, s10 = U[2].y, c1 = U[3].x;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (j & (1 << Q))
+            continue;
+        const double2 x0 = v[j], x1 = v[j | (1 << Q)];
+        v[j] = make_double2(fma(c0, x0.x, -s01 * x1.y), fma(c0, x0.y, s01 * x1.x));
+        v[j | (1 << Q)] = make_double2(fma(c1, x1.x, -s10 * x0.y), fma(c1, x1.y, s10 * x0.x));
+    }
+}
+
+template <int NV, int A, int B>  // A < B: matrix bit 0 <-> block qubit A, bit 1 <-> B
+__device__ __forceinline__ void rb_u2(double2 (&v)[NV], const double2* M) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (j & ((1 << A) | (1 << B)))
+            continue;
+        const int i1 = j | (1 << A), i2 = j | (1 << B), i3 = j | (1 << A) | (1 << B);
+        const double2 x0 = v[j], x1 = v[i1], x2 = v[i2], x3 = v[i3];
+        double2 y[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double2 acc = make_double2(0.0, 0.0);
+            cmac(acc, M[4 * r + 0], x0);
+            cmac(acc, M[4 * r + 1], x1);
+            cmac(acc, M[4 * r + 2], x2);
+            cmac(acc, M[4 * r + 3], x3);
+            y[r] = acc;
+        }
+        v[j] = y[0];
+        v[i1] = y[1];
+        v[i2] = y[2];
+        v[i3] = y[3];
+    }
+}
+
+// CX on (C, T) swaps members with bit C = 1, i.e. registers whose bit C
+// differs from the rotation bit r_C.
+template <int NV, int C, int T>
+__device__ __forceinline__ void rb_cx(double2 (&v)[NV], uint32_t r) {
+    const bool rc = (r >> C) & 1u;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (j & (1 << T))
+            continue;
+        const bool fire = (((j >> C) & 1) != 0) != rc;
+        const double2 x0 = v[j], x1 = v[j | (1 << T)];
+        v[j] = fire ? x1 : x0;
+        v[j | (1 << T)] = fire ? x0 : x1;
+    }
+}
+
+template <int NV>
+__device__ __forceinline__ void rb_diag(double2 (&v)[NV], const double2* D, uint32_t r) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+        v[j] = cmul(D[j ^ r], v[j]);
+}
+
+#define RB_CODE(kind, a, b) (((kind) << 4) | ((a) << 2) | (b))
+
+template <int NV>
+__device__ __forceinline__ void rb_apply(double2 (&v)[NV], const DevPrim pr, const double2* m, uint32_t r) {
+    const uint32_t ra = (r >> pr.a) & 1u, rb = (r >> pr.b) & 1u;
+    const double2* m1 = m + 4 * ra;                 // U1 variant (U or XUX)
+    const double2* m2 = m + 16 * (ra | (rb << 1));  // U2 variant
+    switch (RB_CODE(pr.kind, pr.a, pr.b)) {
+    case RB_CODE(QSV_PRIM_U1, 0, 0): rb_u1<NV, 0>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1, 1, 0): rb_u1<NV, 1>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1, 2, 0): rb_u1<NV, 2>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1R, 0, 0): rb_u1r<NV, 0>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1R, 1, 0): rb_u1r<NV, 1>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1R, 2, 0): rb_u1r<NV, 2>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1I, 0, 0): rb_u1i<NV, 0>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1I, 1, 0): rb_u1i<NV, 1>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U1I, 2, 0): rb_u1i<NV, 2>(v, m1); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 1): rb_u2<NV, 0, 1>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 0, 2): rb_u2<NV, 0, 2>(v, m2); break;
+    case RB_CODE(QSV_PRIM_U2, 1, 2): rb_u2<NV, 1, 2>(v, m2); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 1): rb_cx<NV, 0, 1>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 0, 2): rb_cx<NV, 0, 2>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 0): rb_cx<NV, 1, 0>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 1, 2): rb_cx<NV, 1, 2>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 0): rb_cx<NV, 2, 0>(v, r); break;
+    case RB_CODE(QSV_PRIM_CX, 2, 1): rb_cx<NV, 2, 1>(v, r); break;
+    default:
+        if constexpr (NV == 16) {
+            switch (RB_CODE(pr.kind, pr.a, pr.b)) {
+            case RB_CODE(QSV_PRIM_U1, 3, 0): rb_u1<NV, 3>(v, m1); return;
+            case RB_CODE(QSV_PRIM_U1R, 3, 0): rb_u1r<NV, 3>(v, m1); return;
+            case RB_CODE(QSV_PRIM_U1I, 3, 0): rb_u1i<NV, 3>(v, m1); return;
+            case RB_CODE(QSV_PRIM_U2, 0, 3): rb_u2<NV, 0, 3>(v, m2); return;
+            case RB_CODE(QSV_PRIM_U2, 1, 3): rb_u2<NV, 1, 3>(v, m2); return;
+            case RB_CODE(QSV_PRIM_U2, 2, 3): rb_u2<NV, 2, 3>(v, m2); return;
+            case RB_CODE(QSV_PRIM_CX, 0, 3): rb_cx<NV, 0, 3>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 1, 3): rb_cx<NV, 1, 3>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 2, 3): rb_cx<NV, 2, 3>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 3, 0): rb_cx<NV, 3, 0>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 3, 1): rb_cx<NV, 3, 1>(v, r); return;
+            case RB_CODE(QSV_PRIM_CX, 3, 2): rb_cx<NV, 3, 2>(v, r); return;
+            default: break;
+            }
+        }
+        rb_diag<NV>(v, m, r);  // QSV_PRIM_DIAG16: 2^KB-entry diagonal
+        break;
+    }
+}
+
+template <int K, int NT, int KB>
+__device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const unsigned char* blob) {
+    constexpr int NV = 1 << KB;
+    uint32_t mk[KB];
+#pragma unroll
+    for (int i = 0; i < KB; ++i)
+        mk[i] = 1u << op.tpos[i];
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    if (threadIdx.x >= groups)
+        return;
+    // this lane's member rotation (bank spreading), as block bits and tile offset
+    const uint32_t r = (op.rot_tab >> (4 * (threadIdx.x & 7))) & 15u;
+    uint32_t offr = 0;
+#pragma unroll
+    for (int i = 0; i < KB; ++i)
+        offr |= ((r >> i) & 1u) ? mk[i] : 0u;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+    const DevPrim* prims = reinterpret_cast<const DevPrim*>(blob + op.prim_byte);
+    const int np = op.nprim;
+#pragma unroll 1
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t base = b | tctrl | offr;
+        double2 v[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            uint32_t o = 0;
+#pragma unroll
+            for (int i = 0; i < KB; ++i)
+                o |= ((j >> i) & 1) ? mk[i] : 0u;
+            v[j] = tile[base ^ o];
+        }
+#pragma unroll 1
+        for (int p = 0; p < np; ++p) {
+            const DevPrim pr = prims[p];
+            rb_apply<NV>(v, pr, reinterpret_cast<const double2*>(blob + pr.data_byte), r);
+        }
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            uint32_t o = 0;
+#pragma unroll
+            for (int i = 0; i < KB; ++i)
+                o |= ((j >> i) & 1) ? mk[i] : 0u;
+            tile[base ^ o] = v[j];
+        }
+        b = next_group(b, F, dstep);
+    }
+}
+
+// ---------------------------------------------------------------- PHASEPROD
+// amp *= c * prod_{q in Q, bit q set} f_q for amplitudes with the controls set.
+// In-tile factors are pre-tabulated over the low 5 tile bits (A[32]) and the
+// high tile bits (B[64]); out-of-tile factors collapse into a CTA constant.
+template <int K, int NT>
+__device__ __forceinline__ void phaseprod_op(double2* tile, const TileOp& op, const unsigned char* blob,
+                                             uint64_t full_base) {
+    const double2* tab = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    const ExtFactor* ext = reinterpret_cast<const ExtFactor*>(blob + op.prim_byte);
+    double2 c = tab[0];
+    for (int i = 0; i < op.nprim; ++i)
+        if ((full_base >> ext[i].bit) & 1ull)
+            c = cmul(c, make_double2(ext[i].re, ext[i].im));
+    const double2* A = tab + 1;
+    const double2* B = tab + 33;
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    if (threadIdx.x >= groups)
+        return;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+#pragma unroll 4
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t idx = b | tctrl;
+        const double2 w = cmul(c, cmul(A[idx & 31u], B[idx >> 5]));
+        tile[idx] = cmul(w, tile[idx]);
+        b = next_group(b, F, dstep);
+    }
+}
+
+__device__ __forceinline__ uint64_t tile_base(uint64_t t, const GeomArg& g) {
+    uint64_t base = t << g.L;
+    for (int i = 0; i < g.nhigh; ++i) {
+        const int h = g.high[i];
+        const uint64_t lo = base & ((1ull << h) - 1ull);
+        base = ((base ^ lo) << 1) | lo;
+    }
+    return base;
+}
+
+// The persistent TMA pipeline of a pass; `ops(tile, blob, full_base)` applies
+// the pass's ops to one SMEM-resident tile (interpreted or JIT-specialised).
+template <int K, int NT, typename Ops>
+__device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const unsigned char* __restrict__ gblob,
+                                              uint32_t blob_bytes, const GeomArg& geom, uint64_t rank_base,
+                                              uint64_t ntiles, Ops&& ops) {
+    constexpr int TILE = 1 << K;
+    extern __shared__ __align__(128) unsigned char smem[];
+    double2* bufs = reinterpret_cast<double2*>(smem);
+    unsigned char* blob = smem + sizeof(double2) * kNumBuf * TILE;
+    __shared__ uint64_t hi_off[1 << QSV_MAX_HIGH];
+    __shared__ __align__(8) uint64_t mbar[kNumBuf];
+
+    const int nh = 1 << geom.nhigh;
+    const int L = geom.L;
+    const uint32_t run_bytes = static_cast<uint32_t>(sizeof(double2)) << L;
+    for (int j = threadIdx.x; j < nh; j += NT) {
+        uint64_t o = 0;
+        for (int i = 0; i < geom.nhigh; ++i)
+            o |= static_cast<uint64_t>((j >> i) & 1) << geom.high[i];
+        hi_off[j] = o;
+    }
+    {
+        const int4* src = reinterpret_cast<const int4*>(gblob);
+        int4* dst = reinterpret_cast<int4*>(blob);
+        for (uint32_t i = threadIdx.x; i < blob_bytes / 16; i += NT)
+            dst[i] = __ldg(src + i);
+    }
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < kNumBuf; ++b)
+            mbar_init(&mbar[b], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint64_t stride = gridDim.x;
+    // Warp 0 drives the TMA bulk engine: lane 0 arms the tile's mbarrier with the
+    // byte count, then the 32 lanes issue the 2^nhigh run copies between them.
+    const int lane = threadIdx.x & 31;
+    auto issue_load = [&](uint64_t t, int b) {
+        const uint64_t base = tile_base(t, geom);
+        double2* dst = bufs + b * TILE;
+        if (lane == 0)
+            mbar_expect_tx(&mbar[b], static_cast<uint32_t>(sizeof(double2) * TILE));
+        __syncwarp();
+        for (int j = lane; j < nh; j += 32)
+            bulk_load(dst + (j << L), psi + base + hi_off[j], run_bytes, &mbar[b]);
+    };
+
+    if (threadIdx.x < 32) {
+        for (int s = 0; s < kNumBuf - 1; ++s) {
+            const uint64_t t = blockIdx.x + s * stride;
+            if (t < ntiles)
+                issue_load(t, s);
+        }
+    }
+
+    int it = 0;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += stride, ++it) {
+        const int b = it % kNumBuf;
+        if (threadIdx.x < 32) {
+            const uint64_t tn = t + (kNumBuf - 1) * stride;
+            if (tn < ntiles) {
+                // Buffer (it + NBUF - 1) % NBUF was last stored from in iteration
+                // it - 1: every lane waits for its own store groups to finish reading.
+                bulk_wait_read_all();
+                __syncwarp();
+                issue_load(tn, (it + kNumBuf - 1) % kNumBuf);
+            }
+        }
+        mbar_wait(&mbar[b], static_cast<uint32_t>((it / kNumBuf) & 1));
+        double2* tile = bufs + b * TILE;
+        const uint64_t base = tile_base(t, geom);
+        const uint64_t full_base = rank_base | base;
+
+        ops(tile, blob, full_base);
+        // Make this thread's generic-proxy SMEM writes visible to the bulk-copy
+        // (async) proxy, then let thread 0 stream the tile back.
+        fence_proxy_async();
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            for (int j = lane; j < nh; j += 32)
+                bulk_store(psi + base + hi_off[j], tile + (j << L), run_bytes);
+            bulk_commit();
+        }
+    }
+    if (threadIdx.x < 32)
+        bulk_wait_all();
+}
+
+
+// ---------------------------------------------------------------- JIT helpers
+// Constant-foldable deposit: insert a zero at every set bit of F (ascending).
+__host__ __device__ constexpr uint32_t cdeposit(uint32_t g, uint32_t F) {
+    for (int p = 0; p < 32; ++p)
+        if ((F >> p) & 1u) {
+            const uint32_t lo = g & ((1u << p) - 1u);
+            g = ((g ^ lo) << 1) | lo;
+        }
+    return g;
+}
+
+__host__ __device__ constexpr int cpopc(uint32_t x) {
+    int c = 0;
+    for (; x; x &= x - 1)
+        ++c;
+    return c;
+}
+
+template <int NV, int C, int T>  // CX without member rotation: pure register renaming
+__device__ __forceinline__ void rb_cx_plain(double2 (&v)[NV]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        if (!((j >> C) & 1) || ((j >> T) & 1))
+            continue;
+        const double2 t = v[j];
+        v[j] = v[j | (1 << T)];
+        v[j | (1 << T)] = t;
+    }
+}
+
+// Register block with every structural quantity a compile-time constant; the
+// generated `body(v, r)` is the block's primitive sequence as straight-line code.
+template <int K, int NT, int KB, uint32_t F, uint32_t TCTRL, uint32_t M0, uint32_t M1, uint32_t M2, uint32_t M3,
+          uint32_t ROT, typename Body>
+__device__ __forceinline__ void jit_rblock(double2* tile, Body&& body) {
+    constexpr int NV = 1 << KB;
+    constexpr uint32_t groups = 1u << (K - cpopc(F));
+    constexpr uint32_t dstep = cdeposit(NT, F);
+    constexpr uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+    if (groups < static_cast<uint32_t>(NT) && threadIdx.x >= groups)
+        return;
+    const uint32_t r = ROT ? ((ROT >> (4 * (threadIdx.x & 7))) & 15u) : 0u;
+    const uint32_t offr = ((r & 1u) ? M0 : 0u) | ((r & 2u) ? M1 : 0u) | ((r & 4u) ? M2 : 0u) | ((r & 8u) ? M3 : 0u);
+    uint32_t b = cdeposit(threadIdx.x, F);
+#pragma unroll 1
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t base = b | TCTRL | offr;
+        double2 v[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            v[j] = tile[base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))];
+        body(v, r);
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            tile[base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))] = v[j];
+        b = ((b | F) + dstep) & ~F;
+    }
+}
+
+} // namespace qsv

@@ -823,6 +823,7 @@ extern "C" int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local, const 
             return QSV_E_CUDA;
         }
         prog->blob_total = all.size();
+        prog->host_blobs = std::move(all);
     }
     *out = prog;
     return QSV_OK;
@@ -890,9 +891,31 @@ extern "C" int qsv_program_free(qsv_program* prog) {
     cudaStreamSynchronize(prog->ctx->stream);
     for (auto& kv : prog->graphs)
         cudaGraphExecDestroy(kv.second);
+    qsv::jit_release(prog);
     if (prog->d_blobs)
         cudaFree(prog->d_blobs);
     delete prog;
+    return QSV_OK;
+}
+
+extern "C" int qsv_program_jit(qsv_program* prog, int max_kernels, double* seconds) {
+    QSV_REQUIRE(prog != nullptr, "qsv_program_jit: null program");
+    QSV_REQUIRE(max_kernels >= 0, "qsv_program_jit: max_kernels must be >= 0");
+    QSV_CUDA(cudaSetDevice(prog->ctx->device));
+    QSV_CUDA(cudaStreamSynchronize(prog->ctx->stream));
+    return qsv::jit_program(prog, max_kernels, seconds);
+}
+
+extern "C" int qsv_program_jit_info(qsv_program* prog, int* kernels, int* steps_jitted) {
+    QSV_REQUIRE(prog != nullptr, "qsv_program_jit_info: null program");
+    if (kernels)
+        *kernels = static_cast<int>(prog->jit_kernels.size());
+    if (steps_jitted) {
+        int c = 0;
+        for (int j : prog->jit_of_step)
+            c += j >= 0;
+        *steps_jitted = c;
+    }
     return QSV_OK;
 }
 
@@ -906,7 +929,10 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
         if (evs)
             QSV_CUDA(cudaEventRecord(evs[i], ctx->stream));
         if (s.desc.kind == QSV_STEP_PASS) {
-            QSV_CUDA(qsv::launch_pass(st, s, prog->d_blobs + s.blob_off, rank_base, ctx->stream));
+            if (!prog->jit_of_step.empty() && prog->jit_of_step[i] >= 0)
+                QSV_CUDA(qsv::launch_jit(prog, st, i, prog->d_blobs + s.blob_off, rank_base, ctx->stream));
+            else
+                QSV_CUDA(qsv::launch_pass(st, s, prog->d_blobs + s.blob_off, rank_base, ctx->stream));
         } else {
             const int rc = qsv::run_swap(st, s.desc.swap_global, s.desc.swap_local, s.desc.chunk_log2,
                                          s.desc.nbuf);

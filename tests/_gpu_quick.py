@@ -12,7 +12,7 @@ for spec in ["qft:5", "random:8:4:2", "random:12:8:2", "hea:12:3:4", "qft:14", "
     n = c.n
     a = rand_state(n)
     ref = O.run_local(c, a)
-    for opts in [pkg.PlanOptions(), pkg.PlanOptions(fusion=False, multi_op_passes=False), pkg.PlanOptions(register_blocks=False, fuse_k=4, tile_k=10), pkg.PlanOptions(fuse_k=5, tile_k=11, pass_budget=400, register_blocks=False), pkg.PlanOptions(rblock_k=4, tile_k=11)]:
+    for opts in [pkg.PlanOptions(), pkg.PlanOptions(jit=False), pkg.PlanOptions(fusion=False, multi_op_passes=False), pkg.PlanOptions(register_blocks=False, fuse_k=4, tile_k=10), pkg.PlanOptions(fuse_k=5, tile_k=11, pass_budget=400, register_blocks=False), pkg.PlanOptions(rblock_k=3, tile_k=10)]:
         e = pkg.Engine(c, opts)
         e.upload(a); e.run(); e.sync()
         got = e.download()
@@ -23,7 +23,7 @@ for spec in ["qft:5", "random:8:4:2", "random:12:8:2", "hea:12:3:4", "qft:14", "
 print("BAD", bad, flush=True)
 for spec in ["random:30:20:2", "qft:30", "hea:30:5:4"]:
     c = pkg.Circuit.generate(spec)
-    for opts in [pkg.PlanOptions(), pkg.PlanOptions(pass_budget=96), pkg.PlanOptions(pass_budget=128), pkg.PlanOptions(pass_budget=48), pkg.PlanOptions(pass_budget=160)]:
+    for opts in [pkg.PlanOptions(jit=False), pkg.PlanOptions(), pkg.PlanOptions(pass_budget=96), pkg.PlanOptions(pass_budget=128), pkg.PlanOptions(pass_budget=160)]:
         e = pkg.Engine(c, opts)
         e.set_basis(0); e.run(); e.sync()
         t = e.time(2)/2
@@ -31,5 +31,5 @@ for spec in ["random:30:20:2", "qft:30", "hea:30:5:4"]:
         hb = sum(s["hbm_bytes"] for s in st)
         fl = sum(s["flops"] for s in st)
         prof = e.profile()
-        print(spec, opts.tile_k, opts.rblock_k, opts.pass_budget, "ms %.1f" % t, "passes", e.stats["passes"], "ops", e.stats["ops_final"], "GB/s %.0f" % (hb/t/1e6), "TF %.2f" % (fl/t/1e9), "min-pass %.2f max %.2f" % (min(prof), max(prof)), flush=True)
+        print(spec, "jit" if opts.jit else "interp", e.jit_info(), opts.pass_budget, "ms %.1f" % t, "passes", e.stats["passes"], "ops", e.stats["ops_final"], "GB/s %.0f" % (hb/t/1e6), "TF %.2f" % (fl/t/1e9), "min-pass %.2f max %.2f" % (min(prof), max(prof)), flush=True)
         e.close()
