@@ -123,6 +123,10 @@ int qsv_apply_fused(qsv_state* st, int k, const int* targets, uint64_t ctrl_mask
                          * primitives (qubit q set) of pool[prim.mat_off]; qubits
                          * anywhere (tile, out-of-tile, rank).  CP/CZ chains (QFT).   */
 
+#define QSV_OP_PARPHASE 5 /* parity phase: amplitudes with all ctrl_mask bits set are
+                         * multiplied by pool[mat_off + parity(index & qmask)]; qmask
+                         * may hold any qubits (a CX ladder . RZ . ladder^-1 string). */
+
 /* Primitive kinds (RBLOCK: a, b index qubits[0..3] of the op; PHASEPROD: a is a
  * physical qubit).  Matrices are complex, row-major, in the pool. */
 #define QSV_PRIM_U1 0      /* 2x2 on block qubit a                                   */
@@ -148,6 +152,7 @@ typedef struct qsv_op_desc {
     int64_t mat_off;       /* offset (complex entries) into the program's pool       */
     int32_t prim_begin;    /* RBLOCK / PHASEPROD: primitives [prim_begin, +nprim)    */
     int32_t nprim;
+    uint64_t qmask;        /* PARPHASE: physical qubits whose parity selects the phase */
 } qsv_op_desc;
 
 /* Step kinds of a program. */

@@ -28,7 +28,7 @@
 
 namespace qsim {
 
-enum class OpKind { Dense, Diag, XPerm, PhaseProd, RBlock, Fence };
+enum class OpKind { Dense, Diag, XPerm, PhaseProd, ParPhase, RBlock, Fence };
 
 // RBLOCK primitive (block-local qubit indices into Op::qubits).
 struct Prim {
@@ -44,7 +44,8 @@ struct Op {
                                 // RBlock: block qubits (<= 4)
     std::vector<int> controls;  // all must be 1
     std::vector<Amp> data;      // Dense: 4^k entries row-major; Diag: 2^k entries;
-                                // PhaseProd: data[0] = constant factor
+                                // PhaseProd: data[0] = constant factor;
+                                // ParPhase: {phase if parity(qubits) even, phase if odd}
     std::vector<std::pair<int, Amp>> factors;  // PhaseProd: multiply by f when qubit is 1
     std::vector<Prim> prims;    // RBlock
     int width = 0;              // RBlock: register-block width (3 or 4 slots)
@@ -93,6 +94,10 @@ struct Plan {
 
 // Classification helpers.
 std::vector<Op> lower(const Circuit& c);
+// CX(c,t) . P . CX(c,t) with P a parity phase whose mask holds t equals the
+// parity phase on mask ^ {c}: collapses CX-ladder / RZ / reverse-ladder Pauli
+// strings (UCCSD) into single diagonal ops that need no tile residency.
+std::vector<Op> reduce_parity(const std::vector<Op>& ops);
 std::vector<Op> fuse_ops(const std::vector<Op>& ops, const PlanOptions& opt);
 // Groups ops acting on <= 4 qubits into register blocks (RBLOCK); a block holds
 // at most max_high qubits at or above min_low (it must fit one pass tile).

@@ -224,6 +224,7 @@ int qsim_circuit_fused(const qsim_circuit* c, const qsim_plan_opts* opts, qsim_c
         const qsim::PlanOptions o = to_opts(opts);
         std::vector<qsim::Op> ops = qsim::lower(c->c);
         if (o.fusion) {
+            ops = qsim::reduce_parity(ops);
             ops = qsim::fuse_ops(ops, o);
             if (o.register_blocks)
                 ops = qsim::form_blocks(ops, o.min_low, std::max(o.tile_k - o.min_low, 0), o.rblock_k);

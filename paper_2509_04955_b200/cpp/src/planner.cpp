@@ -37,7 +37,9 @@ bool matrix_is_x(const GateMatrix& m) {
            m.at(0, 1) == Amp{1.0, 0.0} && m.at(1, 0) == Amp{1.0, 0.0};
 }
 
-bool diag_like(const Op& o) { return o.kind == OpKind::Diag || o.kind == OpKind::PhaseProd; }
+bool diag_like(const Op& o) {
+    return o.kind == OpKind::Diag || o.kind == OpKind::PhaseProd || o.kind == OpKind::ParPhase;
+}
 
 // Every qubit an op reads or writes (its DAG footprint).
 std::vector<int> footprint(const Op& o) {
@@ -62,6 +64,12 @@ Amp diag_value(const Op& o, Bit&& bit) {
         for (std::size_t i = 0; i < o.qubits.size(); ++i)
             lin |= static_cast<std::size_t>(bit(o.qubits[i])) << i;
         return o.data[lin];
+    }
+    if (o.kind == OpKind::ParPhase) {
+        int par = 0;
+        for (int q : o.qubits)
+            par ^= bit(q) & 1;
+        return o.data[par];
     }
     Amp v = o.data[0];
     for (const auto& f : o.factors)
@@ -162,7 +170,9 @@ std::optional<std::pair<Factors, Amp>> as_phaseprod(const Op& o, const std::vect
             extra.push_back(c);
     Factors f;
     Amp c0{1.0, 0.0};
-    if (o.kind == OpKind::PhaseProd) {
+    if (o.kind == OpKind::ParPhase && o.qubits.size() != 1) {
+        return std::nullopt;
+    } else if (o.kind == OpKind::PhaseProd) {
         f = o.factors;
         c0 = o.data[0];
     } else if (o.qubits.empty()) {
@@ -293,7 +303,7 @@ bool is_identity(const Op& o) {
                 return false;
         return true;
     }
-    if (o.kind == OpKind::Diag) {
+    if (o.kind == OpKind::Diag || o.kind == OpKind::ParPhase) {
         for (const Amp& a : o.data)
             if (a != Amp{1.0, 0.0})
                 return false;
@@ -313,6 +323,7 @@ bool block_eligible(const Op& o, int width) {
     case OpKind::Dense: return o.qubits.size() + o.controls.size() <= 2;
     case OpKind::XPerm: return o.controls.size() <= 1;
     case OpKind::Diag:
+    case OpKind::ParPhase:
     case OpKind::PhaseProd: return static_cast<int>(footprint(o).size()) <= width;
     default: return false;
     }
@@ -390,6 +401,7 @@ double op_cost(const Op& o) {
     case OpKind::Dense: return 4.0 * std::ldexp(1.0, static_cast<int>(o.qubits.size())) * ctl + 3.0;
     case OpKind::Diag: return 4.0 * ctl + 3.0;
     case OpKind::PhaseProd: return 8.0 * ctl + 3.0;
+    case OpKind::ParPhase: return 4.0 * ctl + 3.0;
     case OpKind::XPerm: return 1.0 * ctl + 2.0;
     case OpKind::RBlock: {
         double c = 3.0;
@@ -400,6 +412,100 @@ double op_cost(const Op& o) {
     case OpKind::Fence: return 0.0;
     }
     return 0.0;
+}
+
+std::vector<Op> reduce_parity(const std::vector<Op>& in) {
+    int nq = 0;
+    for (const Op& o : in)
+        for (int q : footprint(o))
+            nq = std::max(nq, q + 1);
+    std::vector<Op> out;
+    out.reserve(in.size());
+    std::vector<char> alive;
+    std::vector<std::vector<int>> wire(static_cast<std::size_t>(nq));  // alive op indices per qubit
+    auto is_cx = [](const Op& o, int& c, int& t) {
+        if (o.kind != OpKind::XPerm || o.controls.size() != 1)
+            return false;
+        c = o.controls[0];
+        t = o.qubits[0];
+        return true;
+    };
+    // parity view of a diagonal op: (mask, p0, p1)
+    auto as_parity = [](const Op& o, std::vector<int>& mask, Amp& p0, Amp& p1) {
+        if (!o.controls.empty())
+            return false;
+        if (o.kind == OpKind::ParPhase) {
+            mask = o.qubits;
+            p0 = o.data[0];
+            p1 = o.data[1];
+            return true;
+        }
+        if (o.kind == OpKind::Diag && o.qubits.size() == 1) {
+            mask = o.qubits;
+            p0 = o.data[0];
+            p1 = o.data[1];
+            return true;
+        }
+        return false;
+    };
+    auto erase_from = [](std::vector<int>& w, int idx) {
+        for (std::size_t i = w.size(); i-- > 0;)
+            if (w[i] == idx) {
+                w.erase(w.begin() + static_cast<std::ptrdiff_t>(i));
+                return;
+            }
+    };
+    for (const Op& b : in) {
+        int c = -1, t = -1;
+        if (is_cx(b, c, t) && wire[t].size() >= 2) {
+            const int y = wire[t].back();
+            const int z = wire[t][wire[t].size() - 2];
+            int zc = -1, zt = -1;
+            std::vector<int> mask;
+            Amp p0, p1;
+            if (alive[y] && alive[z] && is_cx(out[z], zc, zt) && zc == c && zt == t &&
+                as_parity(out[y], mask, p0, p1) && contains(mask, t)) {
+                const bool c_in = contains(mask, c);
+                const auto& wc = wire[c];
+                const bool c_ok = c_in ? (wc.size() >= 2 && wc.back() == y && wc[wc.size() - 2] == z)
+                                       : (!wc.empty() && wc.back() == z);
+                if (c_ok) {
+                    Op p;
+                    p.kind = OpKind::ParPhase;
+                    p.qubits = mask;
+                    if (c_in)
+                        p.qubits.erase(std::find(p.qubits.begin(), p.qubits.end(), c));
+                    else
+                        p.qubits.push_back(c);
+                    std::sort(p.qubits.begin(), p.qubits.end());
+                    p.data = {p0, p1};
+                    p.first_gate = std::min(out[z].first_gate, out[y].first_gate);
+                    p.last_gate = b.last_gate;
+                    p.ngates = out[z].ngates + out[y].ngates + b.ngates;
+                    alive[z] = 0;
+                    erase_from(wire[c], z);
+                    erase_from(wire[t], z);
+                    if (c_in)
+                        erase_from(wire[c], y);
+                    else
+                        wire[c].push_back(y);
+                    out[y] = std::move(p);
+                    continue;
+                }
+            }
+        }
+        const int idx = static_cast<int>(out.size());
+        out.push_back(b);
+        alive.push_back(1);
+        for (int q : footprint(b))
+            wire[q].push_back(idx);
+    }
+    std::vector<Op> res;
+    res.reserve(out.size());
+    for (std::size_t i = 0; i < out.size(); ++i)
+        if (alive[i])
+            res.push_back(std::move(out[i]));
+    return res;
 }
 
 std::vector<Op> lower(const Circuit& c) {
@@ -696,6 +802,13 @@ struct Packer {
                 d.qubits[i] = pos[o.qubits[i]];
             d.mat_off = put(o.data);
             break;
+        case OpKind::ParPhase:
+            d.kind = QSV_OP_PARPHASE;
+            d.k = 0;
+            for (int q : o.qubits)
+                d.qmask |= 1ull << pos[q];
+            d.mat_off = put(o.data);
+            break;
         case OpKind::PhaseProd:
             d.kind = QSV_OP_PHASEPROD;
             d.k = 0;
@@ -750,6 +863,7 @@ struct Packer {
         }
         case OpKind::Diag: b += o.data.size() * 16 + 96; break;
         case OpKind::PhaseProd: b += 97 * 16 + o.factors.size() * 32; break;
+        case OpKind::ParPhase: b += 32; break;
         case OpKind::RBlock:
             for (const Prim& p : o.prims)
                 b += 8 + (p.kind == QSV_PRIM_U1 ? 64 : (p.kind == QSV_PRIM_CX ? 0 : 256)) + 16;
@@ -828,6 +942,7 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     std::vector<Op> ops = lower(c);
     plan.stats.ops_lowered = ops.size();
     if (opt.fusion) {
+        ops = reduce_parity(ops);
         PlanOptions fo = opt;
         fo.tile_k = std::min(opt.tile_k, plan.n_local);
         fo.min_low = std::min(opt.min_low, fo.tile_k);
@@ -960,6 +1075,20 @@ Circuit ops_to_circuit(int n, const std::vector<Op>& ops) {
                 add_matrix(o.qubits, o.controls, m);
             }
             break;
+        case OpKind::ParPhase: {
+            // parity into the last mask qubit with a CX ladder, the phase, ladder back
+            const std::vector<int>& m = o.qubits;
+            if (m.empty()) {
+                add_phase({}, o.data[0], 0);
+                break;
+            }
+            for (std::size_t i = 0; i + 1 < m.size(); ++i)
+                add_matrix({m[i + 1]}, {m[i]}, {0.0, 1.0, 1.0, 0.0});
+            add_matrix({m.back()}, {}, {o.data[0], 0.0, 0.0, o.data[1]});
+            for (std::size_t i = m.size() - 1; i-- > 0;)
+                add_matrix({m[i + 1]}, {m[i]}, {0.0, 1.0, 1.0, 0.0});
+            break;
+        }
         case OpKind::PhaseProd:
             add_phase(o.controls, o.data[0], 0);
             for (const auto& f : o.factors) {

@@ -24,6 +24,7 @@ typedef unsigned long long uint64_t;
 #define QSV_OP_XPERM 2
 #define QSV_OP_RBLOCK 3
 #define QSV_OP_PHASEPROD 4
+#define QSV_OP_PARPHASE 5
 #define QSV_PRIM_U1 0
 #define QSV_PRIM_U2 1
 #define QSV_PRIM_CX 2
@@ -57,7 +58,8 @@ struct TileOp {
     uint32_t prim_byte;           // RBLOCK: DevPrim list; PHASEPROD: ExtFactor list
     int32_t nprim;
     uint32_t rot_tab;             // RBLOCK: 4-bit member rotation per lane & 7 (bank spreading)
-    uint32_t pad2[3];
+    uint32_t pad2;
+    uint64_t xmask;               // PARPHASE: out-of-tile qubits of the parity mask (full index)
 };
 static_assert(sizeof(TileOp) % 16 == 0, "TileOp must keep 16-B alignment in the blob");
 

@@ -159,6 +159,9 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
         case QSV_OP_PHASEPROD:
             o << "  qsv::phaseprod_op<" << K << ", " << NT << ">(tile, " << opref << ", blob, full_base);\n";
             break;
+        case QSV_OP_PARPHASE:
+            o << "  qsv::parphase_op<" << K << ", " << NT << ">(tile, " << opref << ", blob, full_base);\n";
+            break;
         case QSV_OP_XPERM:
             o << "  qsv::xperm_op<" << K << ", " << NT << ">(tile, " << opref << ");\n";
             break;

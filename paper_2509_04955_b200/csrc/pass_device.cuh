@@ -477,6 +477,33 @@ __device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const
     }
 }
 
+// ---------------------------------------------------------------- PARPHASE
+// amp *= P[parity(index & mask)] for amplitudes with the controls set; the
+// out-of-tile part of the parity is CTA-uniform.
+template <int K, int NT>
+__device__ __forceinline__ void parphase_op(double2* tile, const TileOp& op, const unsigned char* blob,
+                                            uint64_t full_base) {
+    const double2* P = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    const uint32_t ext = static_cast<uint32_t>(__popcll(full_base & op.xmask)) & 1u;
+    const double2 p0 = P[ext], p1 = P[ext ^ 1u];
+    const uint32_t tmask = op.tmask;
+    const int nfix = op.nfix;
+    const uint32_t tctrl = op.tctrl;
+    const uint32_t F = op.fmask;
+    const uint32_t groups = 1u << (K - nfix);
+    if (threadIdx.x >= groups)
+        return;
+    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+#pragma unroll 4
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t idx = b | tctrl;
+        tile[idx] = cmul((__popc(idx & tmask) & 1) ? p1 : p0, tile[idx]);
+        b = next_group(b, F, dstep);
+    }
+}
+
 // ---------------------------------------------------------------- PHASEPROD
 // amp *= c * prod_{q in Q, bit q set} f_q for amplitudes with the controls set.
 // In-tile factors are pre-tabulated over the low 5 tile bits (A[32]) and the

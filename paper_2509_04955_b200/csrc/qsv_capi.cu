@@ -639,6 +639,22 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
             pl.data = std::move(tab);
             t.nprim = static_cast<int32_t>(pl.ext.size());
             flops += 18.0 * amps * frac;
+        } else if (od.kind == QSV_OP_PARPHASE) {
+            QSV_REQUIRE(od.k == 0, "op: PARPHASE takes its qubits in qmask (k = 0)");
+            QSV_REQUIRE((od.qmask & ~full_mask) == 0, "op: PARPHASE mask bit >= n_total");
+            QSV_REQUIRE((od.qmask & od.ctrl_mask) == 0, "op: PARPHASE mask overlaps a control");
+            QSV_REQUIRE(od.mat_off >= 0 && static_cast<size_t>(od.mat_off) + 2 <= pool_len,
+                        "op: PARPHASE phases outside the pool");
+            for (int q = 0; q < n_total; ++q) {
+                if (!(od.qmask >> q & 1))
+                    continue;
+                if (q < n_local && tpos_of[q] >= 0)
+                    t.tmask |= 1u << tpos_of[q];
+                else
+                    t.xmask |= 1ull << q;
+            }
+            pl.data.assign(pool + 2 * od.mat_off, pool + 2 * (od.mat_off + 2));
+            flops += 6.0 * amps * frac;
         } else if (od.kind == QSV_OP_DIAG) {
             QSV_REQUIRE(od.k >= 0 && od.k <= QSV_MAX_DIAG_K, "op: diagonal arity must be in [0, 8]");
             const int D = 1 << od.k;

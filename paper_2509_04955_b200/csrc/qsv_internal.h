@@ -13,7 +13,8 @@
 
 #include "device_types.h"
 
-static_assert(QSV_OP_RBLOCK == 3 && QSV_OP_PHASEPROD == 4 && QSV_PRIM_U1I == 6 && QSV_MAX_HIGH == 8,
+static_assert(QSV_OP_RBLOCK == 3 && QSV_OP_PHASEPROD == 4 && QSV_OP_PARPHASE == 5 && QSV_PRIM_U1I == 6 &&
+                  QSV_MAX_HIGH == 8,
               "device_types.h constants must mirror include/qsv.h");
 
 namespace qsv {

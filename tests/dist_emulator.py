@@ -18,7 +18,8 @@ class Step(C.Structure):
 
 class Op(C.Structure):
     _fields_ = [("kind", C.c_int32), ("k", C.c_int32), ("qubits", C.c_int32 * 8), ("ctrl_mask", C.c_uint64),
-                ("mat_off", C.c_int64), ("prim_begin", C.c_int32), ("nprim", C.c_int32)]
+                ("mat_off", C.c_int64), ("prim_begin", C.c_int32), ("nprim", C.c_int32),
+                ("qmask", C.c_uint64)]
 
 
 class Prim(C.Structure):
@@ -79,6 +80,13 @@ def apply_op(psi, op, prims, pool, rank, n_local):
         for i, qq in enumerate(q):
             e |= (((full[bases] >> np.uint64(qq)) & np.uint64(1)).astype(np.int64)) << i
         psi[bases] *= pool[op.mat_off + e]
+    elif kind == 5:  # PARPHASE
+        bases, full = _groups(l, rank, [], op.ctrl_mask, n_local)
+        par = np.zeros(bases.size, dtype=np.int64)
+        for q in range(64):
+            if op.qmask >> q & 1:
+                par ^= ((full[bases] >> np.uint64(q)) & np.uint64(1)).astype(np.int64)
+        psi[bases] *= pool[op.mat_off + par]
     elif kind == 4:  # PHASEPROD
         bases, full = _groups(l, rank, [], op.ctrl_mask, n_local)
         w = np.full(bases.size, pool[op.mat_off], dtype=np.complex128)

@@ -59,7 +59,8 @@ def test_program_validate_rejects_bad_programs():
 
     class Op(C.Structure):
         _fields_ = [("kind", C.c_int32), ("k", C.c_int32), ("qubits", C.c_int32 * 8), ("ctrl_mask", C.c_uint64),
-                    ("mat_off", C.c_int64), ("prim_begin", C.c_int32), ("nprim", C.c_int32)]
+                    ("mat_off", C.c_int64), ("prim_begin", C.c_int32), ("nprim", C.c_int32),
+                ("qmask", C.c_uint64)]
 
     pool = (C.c_double * 8)(0.0, 0.0, 1.0, 0.0, 1.0, 0.0, 0.0, 0.0)  # X
     op = Op(kind=0, k=1, ctrl_mask=0, mat_off=0)
