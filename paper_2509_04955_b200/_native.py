@@ -136,7 +136,7 @@ class PlanOptions:
     fuse_k: int = 2
     fusion: bool = True
     multi_op_passes: bool = True
-    chunk_log2: int = 22
+    chunk_log2: int = 26
     nbuf: int = 2
     pass_budget: float = 72.0
     register_blocks: bool = True
