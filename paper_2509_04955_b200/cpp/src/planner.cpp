@@ -967,44 +967,89 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     }
 
     Packer pk(opt, c.n, plan.n_local, plan);
-    // next tile use of each logical qubit, for swap-victim selection (Belady)
     const int nops = static_cast<int>(ops.size());
-    std::vector<std::vector<int>> uses(c.n);
-    for (int i = 0; i < nops; ++i)
-        for (int q : local_needs(ops[i]))
-            uses[q].push_back(i);
-    std::vector<std::size_t> cursor(c.n, 0);
-    auto next_use = [&](int q, int from) {
-        auto& u = uses[q];
-        std::size_t& k = cursor[q];
-        while (k < u.size() && u[k] < from)
-            ++k;
-        return k < u.size() ? u[k] : std::numeric_limits<int>::max();
-    };
-    for (int i = 0; i < nops; ++i) {
-        const Op& o = ops[i];
-        const std::vector<int> need = local_needs(o);
-        for (int q : need) {
-            if (pk.pos[q] < plan.n_local)
-                continue;
-            int best = -1;
-            long long best_score = -1;
-            for (int l = 0; l < c.n; ++l) {
-                const int p = pk.pos[l];
-                if (p >= plan.n_local || contains(need, l) || p < pk.Lmin)
-                    continue;
-                const long long nu = next_use(l, i);
-                const long long score = nu * 64 + p;
-                if (score > best_score) {
-                    best_score = score;
-                    best = l;
+    if (plan.n_local == c.n) {
+        for (const Op& o : ops)
+            pk.add(o);
+    } else {
+        // Local-first list scheduling over the dependency DAG (multi-GPU): run
+        // every ready op whose tile qubits are all local; only when none is ready
+        // bring the needed global qubits in with BBOP swaps, evicting the local
+        // qubits with the fewest remaining uses (finished qubits first).
+        std::vector<std::vector<int>> fp(nops);
+        std::vector<int> npred(nops, 0);
+        std::vector<std::vector<int>> succ(nops);
+        std::vector<int> last(static_cast<std::size_t>(c.n), -1);
+        for (int i = 0; i < nops; ++i) {
+            fp[i] = footprint(ops[i]);
+            std::vector<int> preds;
+            for (int q : fp[i]) {
+                if (last[q] >= 0 && !contains(preds, last[q]))
+                    preds.push_back(last[q]);
+                last[q] = i;
+            }
+            npred[i] = static_cast<int>(preds.size());
+            for (int p : preds)
+                succ[p].push_back(i);
+        }
+        std::vector<int> remaining(static_cast<std::size_t>(c.n), 0);
+        for (int i = 0; i < nops; ++i)
+            for (int q : local_needs(ops[i]))
+                ++remaining[q];
+        std::vector<int> ready;
+        for (int i = 0; i < nops; ++i)
+            if (npred[i] == 0)
+                ready.push_back(i);
+        auto is_local = [&](int i) {
+            for (int q : local_needs(ops[i]))
+                if (pk.pos[q] >= plan.n_local)
+                    return false;
+            return true;
+        };
+        int done = 0;
+        while (done < nops) {
+            int pick = -1;
+            for (int i : ready)
+                if (is_local(i) && (pick < 0 || i < pick))
+                    pick = i;
+            if (pick < 0) {
+                pick = *std::min_element(ready.begin(), ready.end());
+                const std::vector<int> need = local_needs(ops[pick]);
+                for (int q : need) {
+                    if (pk.pos[q] < plan.n_local)
+                        continue;
+                    // victims: local, not needed by this op, preferably outside the low
+                    // run (contiguous swap chunks) and outside the open pass's tile
+                    int best = -1;
+                    for (int relax = 0; relax < 2 && best < 0; ++relax) {
+                        long long best_score = std::numeric_limits<long long>::max();
+                        for (int l = 0; l < c.n; ++l) {
+                            const int p = pk.pos[l];
+                            if (p >= plan.n_local || contains(need, l))
+                                continue;
+                            if (relax == 0 && (p < pk.Lmin || contains(pk.targets, p)))
+                                continue;
+                            const long long score = static_cast<long long>(remaining[l]) * 64 - p;
+                            if (score < best_score) {
+                                best_score = score;
+                                best = l;
+                            }
+                        }
+                    }
+                    if (best < 0)
+                        throw std::logic_error("planner: no swap victim available");
+                    pk.swap(pk.pos[q], pk.pos[best]);
                 }
             }
-            if (best < 0)
-                throw std::logic_error("planner: no swap victim available");
-            pk.swap(pk.pos[q], pk.pos[best]);
+            ready.erase(std::find(ready.begin(), ready.end(), pick));
+            pk.add(ops[pick]);
+            for (int q : local_needs(ops[pick]))
+                --remaining[q];
+            ++done;
+            for (int sI : succ[pick])
+                if (--npred[sI] == 0)
+                    ready.push_back(sI);
         }
-        pk.add(o);
     }
     pk.close_pass();
     // restore the logical qubit order so the final state is in standard layout
