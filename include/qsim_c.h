@@ -77,6 +77,14 @@ int qsim_circuit_fused(const qsim_circuit* c, const qsim_plan_opts* opts, qsim_c
 int qsim_circuit_plan(const qsim_circuit* c, const qsim_plan_opts* opts, int n_local, int rank,
                       qsim_plan_stats* stats);
 void qsim_circuit_free(qsim_circuit* c);
+/* OpenQASM 2.0 subset (qsim/qasm.hpp).  parse: text of len bytes (need not be
+ * NUL-terminated); on a syntax/semantic error returns QSV_E_ARG with the 1-based location in
+ * *line / *col (either may be NULL) and the message in qsim_last_error().
+ * emit: writes at most cap bytes (NUL-terminated when it fits) and the full length without
+ * the NUL to *needed; call with cap = 0 to size the buffer.  matrix_export != 0 writes gates
+ * outside the mnemonic set as `// qsv-unitary` directives (otherwise QSV_E_ARG). */
+int qsim_circuit_parse_qasm(const char* text, int64_t len, qsim_circuit** out, int* line, int* col);
+int qsim_circuit_emit_qasm(const qsim_circuit* c, int matrix_export, char* buf, int64_t cap, int64_t* needed);
 /* Exports the device program of the plan (include/qsv.h structures).  Call
  * with NULL arrays to get the counts, then again with buffers of that size. */
 int qsim_plan_export(const qsim_circuit* c, const qsim_plan_opts* opts, int n_local, int* nsteps, int* nops,

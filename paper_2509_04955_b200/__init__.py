@@ -15,6 +15,7 @@ from ._native import (  # noqa: F401
     Circuit,
     Engine,
     PlanOptions,
+    QasmError,
     QsvError,
     lib_paths,
     load_qsim,
@@ -26,6 +27,7 @@ __all__ = [
     "Circuit",
     "Engine",
     "PlanOptions",
+    "QasmError",
     "QsvError",
     "lib_paths",
     "load_qsim",

@@ -114,6 +114,15 @@ def load_qsim() -> C.CDLL:
     return _qsim
 
 
+class QasmError(ValueError):
+    """A QASM parse error with its 1-based location (qsim::QasmError)."""
+
+    def __init__(self, message: str, line: int, column: int):
+        super().__init__(message)
+        self.line = line
+        self.column = column
+
+
 def _check(rc: int, what: str, lib=None) -> None:
     if rc == QSV_OK:
         return
@@ -175,6 +184,32 @@ class Circuit:
         h = C.c_void_p()
         _check(load_qsim().qsim_circuit_new(n, C.byref(h)), "qsim_circuit_new")
         return cls(h.value)
+
+    @classmethod
+    def from_qasm(cls, text: str | bytes) -> "Circuit":
+        """parse_qasm; raises QasmError(line, column) on bad input."""
+        b = text.encode() if isinstance(text, str) else bytes(text)
+        h = C.c_void_p()
+        line = C.c_int()
+        col = C.c_int()
+        L = load_qsim()
+        rc = L.qsim_circuit_parse_qasm(C.c_char_p(b), C.c_int64(len(b)), C.byref(h), C.byref(line), C.byref(col))
+        if rc != QSV_OK:
+            msg = (L.qsim_last_error() or b"").decode(errors="replace")
+            if rc == QSV_E_ARG:
+                raise QasmError(msg, line.value, col.value)
+            _check(rc, "parse_qasm")
+        return cls(h.value)
+
+    def to_qasm(self, matrix_export: bool = False) -> str:
+        """emit_qasm (SPEC:172-179)."""
+        L = load_qsim()
+        need = C.c_int64()
+        _check(L.qsim_circuit_emit_qasm(self._h, int(matrix_export), None, C.c_int64(0), C.byref(need)), "emit_qasm")
+        buf = C.create_string_buffer(need.value + 1)
+        _check(L.qsim_circuit_emit_qasm(self._h, int(matrix_export), buf, C.c_int64(need.value + 1), C.byref(need)),
+               "emit_qasm")
+        return buf.value.decode()
 
     def add(self, mnemonic: str, qubits, params=()) -> "Circuit":
         q = (C.c_int * len(qubits))(*qubits)

@@ -37,7 +37,8 @@ Circuit gen_random(int n, int depth, std::uint64_t seed);
 Circuit gen_uccsd_ladder(int n, std::uint64_t target_cx, std::uint64_t seed);
 
 // "qft:n" | "qaoa:n:p:seed" | "hea:n:layers:seed" | "random:n:depth:seed" |
-// "uccsd:n:target_cx:seed" (SPEC:504 generator specs).
+// "uccsd:n:target_cx:seed" (SPEC:504 generator specs) | "qasm:<path>" (parse_qasm_file,
+// qsim/qasm.hpp).
 Circuit generate(const std::string& spec);
 
 } // namespace qsim

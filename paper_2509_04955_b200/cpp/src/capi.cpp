@@ -10,7 +10,9 @@
 #include "qsim/generators.hpp"
 #include "qsim/memtrack.hpp"
 #include "qsim/planner.hpp"
+#include "qsim/qasm.hpp"
 
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -200,6 +202,42 @@ int qsim_circuit_export(const qsim_circuit* c, qsim_gate_rec* recs, double* pool
                 }
             }
             recs[i] = r;
+        }
+        return QSV_OK;
+    });
+}
+
+int qsim_circuit_parse_qasm(const char* text, int64_t len, qsim_circuit** out, int* line, int* col) {
+    if (line)
+        *line = 0;
+    if (col)
+        *col = 0;
+    return guard([&] {
+        REQUIRE(out && len >= 0 && (text || len == 0), "qsim_circuit_parse_qasm: bad argument");
+        try {
+            *out = new qsim_circuit{qsim::parse_qasm(std::string_view(text ? text : "", static_cast<std::size_t>(len)))};
+        } catch (const qsim::QasmError& e) {
+            if (line)
+                *line = e.line();
+            if (col)
+                *col = e.column();
+            throw;
+        }
+        return QSV_OK;
+    });
+}
+
+int qsim_circuit_emit_qasm(const qsim_circuit* c, int matrix_export, char* buf, int64_t cap, int64_t* needed) {
+    return guard([&] {
+        REQUIRE(c && needed && cap >= 0 && (buf || cap == 0), "qsim_circuit_emit_qasm: bad argument");
+        qsim::QasmEmitOptions o;
+        o.matrix_export = matrix_export != 0;
+        const std::string s = qsim::emit_qasm(c->c, o);
+        *needed = static_cast<int64_t>(s.size());
+        if (cap > 0) {
+            const std::size_t n = std::min<std::size_t>(s.size(), static_cast<std::size_t>(cap - 1));
+            std::memcpy(buf, s.data(), n);
+            buf[n] = '\0';
         }
         return QSV_OK;
     });

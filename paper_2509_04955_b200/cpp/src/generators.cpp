@@ -1,5 +1,6 @@
 // Definitions for qsim/generators.hpp.
 #include "qsim/generators.hpp"
+#include "qsim/qasm.hpp"
 
 #include <cmath>
 #include <numbers>
@@ -145,6 +146,8 @@ Circuit gen_uccsd_ladder(int n, std::uint64_t target_cx, std::uint64_t seed) {
 }
 
 Circuit generate(const std::string& spec) {
+    if (spec.rfind("qasm:", 0) == 0)
+        return parse_qasm_file(spec.substr(5));  // OpenQASM 2.0 file
     std::vector<std::string> f;
     std::stringstream ss(spec);
     std::string item;
@@ -170,7 +173,7 @@ Circuit generate(const std::string& spec) {
     if (k == "hea") return gen_hea(static_cast<int>(num(1, 8)), static_cast<int>(num(2, 5)), num(3, 4));
     if (k == "random") return gen_random(static_cast<int>(num(1, 8)), static_cast<int>(num(2, 20)), num(3, 2));
     if (k == "uccsd") return gen_uccsd_ladder(static_cast<int>(num(1, 8)), num(2, 100000), num(3, 3));
-    throw std::invalid_argument("unknown generator '" + k + "' (qft|qaoa|hea|random|uccsd)");
+    throw std::invalid_argument("unknown generator '" + k + "' (qft|qaoa|hea|random|uccsd|qasm:<file>)");
 }
 
 } // namespace qsim

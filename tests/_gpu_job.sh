@@ -17,4 +17,4 @@ best = max(((float(m.group(2)), int(m.group(1))) for m in (re.match(r"(\d+) ([\d
 print(best[1])
 PY
 ) && echo "heaviest pass $IDX" && \
-ncu --set full --import-source on --clock-control none -k regex:pass_kernel -s $IDX -c 1 -o gpurun_out/prof_full python tests/_prof.py random:30:20:2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+ncu --set full --import-source on --clock-control none -k regex:"qsv_jit|pass_kernel" -s $IDX -c 1 -o gpurun_out/prof_full python tests/_prof.py random:30:20:2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
