@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--fusion", default="on", choices=["on", "off"])
     ap.add_argument("--tile-k", type=int, default=None)
     ap.add_argument("--budget", type=float, default=None)
+    ap.add_argument("--relabel", type=int, default=1, choices=[0, 1, 2],
+                    help="tile-qubit relabelling: 0 off, 1 auto (kept when it saves passes), 2 always")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of CPU work per reference step")
@@ -212,10 +214,15 @@ def main():
         opts.tile_k = args.tile_k
     if args.budget:
         opts.pass_budget = args.budget
+    opts.relabel = args.relabel
     circ = pkg.Circuit.generate(args.workload)
     n = circ.n
     t_plan0 = time.perf_counter()
     eng = pkg.Engine(circ, opts, device=local if world > 1 else 0, rank=rank, nranks=world, comm_id=comm_id)
+    jit = eng.jit_info()
+    if opts.jit and jit["kernels"] == 0:
+        print("bench: WARNING specialised (NVRTC) pass kernels unavailable; interpreter kernel in use",
+              file=sys.stderr)
     plan_s = time.perf_counter() - t_plan0
     st = eng.stats
     steps_info = eng.steps()
@@ -354,6 +361,7 @@ def main():
         "config": {
             "workload": args.workload, "qubits": n, "local_qubits": n_local, "ranks": world,
             "fusion": args.fusion, "tile_k": opts.tile_k, "pass_budget": opts.pass_budget,
+            "relabel": args.relabel, "jit_kernels": jit["kernels"], "jit_seconds": round(jit["seconds"], 2),
             "gates": gates, "ops_after_fusion": st["ops_fused"], "ops_final": st["ops_final"],
             "passes": st["passes"], "swaps": st["swaps"], "plan_seconds": plan_s,
             "l2": "state (16 B x 2^n) >> 126 MB L2; no flush needed",

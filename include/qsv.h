@@ -167,6 +167,11 @@ typedef struct qsv_step_desc {
     int32_t nhigh;
     int32_t high[QSV_MAX_HIGH];
     int32_t op_begin, op_count;
+    /* PASS, optional relabel applied after the ops: tile bit i (0..L-1 = the low run,
+     * L.. = high[] in order) moves to tile bit relabel[i], i.e. the physical qubit
+     * slots of the tile are permuted in place (a bijection on the tile's bits). */
+    int32_t has_relabel;
+    int32_t relabel[16];
     /* SWAP: exchange physical global qubit g with local qubit v, moving 2^chunk_log2
      * amplitudes per message with nbuf staging buffers (BBOP b and B). */
     int32_t swap_global, swap_local, chunk_log2, nbuf;
@@ -196,6 +201,12 @@ int qsv_program_jit_info(qsv_program* prog, int* kernels, int* steps_jitted);
 int qsv_program_validate(int n_total, int n_local, int rank, const qsv_step_desc* steps, int nsteps,
                          const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims, int nprims,
                          const double* pool, size_t pool_len);
+/* Host-only: qsv_program_validate plus an NVRTC compile (sm_100a cubin) of the
+ * program's distinct specialised pass kernels, as qsv_program_jit would build them;
+ * *kernels receives their number.  No device needed (CPU tests of the JIT path). */
+int qsv_program_jit_check(int n_total, int n_local, int rank, const qsv_step_desc* steps, int nsteps,
+                          const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims, int nprims,
+                          const double* pool, size_t pool_len, int max_kernels, int* kernels);
 /* Enqueues every step of the program on the context stream (a CUDA graph when
  * the program has no collective steps).  Replaces run_local and
  * run_distributed's dispatch loop. */

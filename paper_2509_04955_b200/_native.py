@@ -56,6 +56,7 @@ class qsim_plan_opts(C.Structure):
         ("pass_budget", C.c_double),
         ("rblock_k", C.c_int32),
         ("jit", C.c_int32),
+        ("relabel", C.c_int32),
     ]
 
 
@@ -151,19 +152,21 @@ class PlanOptions:
     register_blocks: bool = True
     rblock_k: int = 4
     jit: bool = True
+    relabel: int = 1  # 0 off, 1 auto (kept when it saves passes), 2 always
 
     @classmethod
     def default(cls) -> "PlanOptions":
         o = qsim_plan_opts()
         load_qsim().qsim_default_opts(C.byref(o))
         return cls(o.tile_k, o.min_low, o.fuse_k, bool(o.fusion), bool(o.multi_op_passes),
-                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k, bool(o.jit))
+                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k, bool(o.jit),
+                   int(o.relabel))
 
     def to_c(self) -> qsim_plan_opts:
         return qsim_plan_opts(self.tile_k, self.min_low, self.fuse_k, int(self.fusion),
                               int(self.multi_op_passes), self.chunk_log2, self.nbuf,
                               int(self.register_blocks), float(self.pass_budget), int(self.rblock_k),
-                              int(self.jit))
+                              int(self.jit), int(self.relabel))
 
 
 class Circuit:

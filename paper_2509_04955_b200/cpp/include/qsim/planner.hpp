@@ -68,6 +68,8 @@ struct PlanOptions {
     int nbuf = 2;             // BBOP buffers B (default 2)
     bool jit = true;          // NVRTC-specialised pass kernels (falls back to the interpreter kernel)
     int jit_max_kernels = 512;  // distinct pass structures compiled at most
+    int relabel = 1;          // tile-qubit relabelling at pass ends: 0 off, 1 auto (kept when it
+                              // saves passes), 2 always (tests)
 };
 
 struct PlanStats {

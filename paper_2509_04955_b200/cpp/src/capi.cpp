@@ -65,6 +65,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.pass_budget = o->pass_budget;
     p.rblock_k = o->rblock_k;
     p.jit = o->jit != 0;
+    p.relabel = o->relabel;
     return p;
 }
 
@@ -118,6 +119,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->pass_budget = p.pass_budget;
     out->rblock_k = p.rblock_k;
     out->jit = p.jit;
+    out->relabel = p.relabel;
 }
 
 int qsim_circuit_generate(const char* spec, qsim_circuit** out) {

@@ -1,6 +1,9 @@
 // Definitions for qsim/planner.hpp.
 #include "qsim/planner.hpp"
 
+#include <cstdio>
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -699,6 +702,10 @@ struct Packer {
     std::vector<qsv_op_desc> cur_ops;
     double cur_cost = 0;
     std::size_t cur_bytes = 0;
+    // in-pass relabelling lookahead (single rank): the op sequence and the next op index
+    const std::vector<Op>* seq = nullptr;
+    std::size_t cursor = 0;
+    int relabels = 0;
 
     Packer(const PlanOptions& o, int n_, int nl, Plan& p) : opt(o), n(n_), n_local(nl), plan(p) {
         K = std::min(opt.tile_k, n_local);
@@ -721,12 +728,136 @@ struct Packer {
         return best;
     }
 
-    void close_pass() {
-        if (cur_ops.empty())
+    // logical qubit -> index of its next tile use at or after `cursor` (large = none)
+    std::vector<long> next_use() const {
+        std::vector<long> nu(static_cast<std::size_t>(n), 1L << 40);
+        int found = 0;
+        for (std::size_t i = cursor; seq && i < seq->size() && i < cursor + 4096 && found < n; ++i) {
+            const Op& o = (*seq)[i];
+            if (o.kind != OpKind::Dense && o.kind != OpKind::XPerm && o.kind != OpKind::RBlock)
+                continue;
+            for (int q : o.qubits)
+                if (nu[q] > static_cast<long>(i)) {
+                    nu[q] = static_cast<long>(i);
+                    ++found;
+                }
+        }
+        return nu;
+    }
+
+    static constexpr long kNever = 1L << 40;
+
+    // Chooses where every tile qubit lives after the pass (tile-bit relabel, applied
+    // by the kernel after the pass's ops).  Policy: the L tile qubits needed soonest
+    // take the low run (it is in every later tile for free); qubits with no further
+    // use go back to their home slot when it is in the tile (so the final state needs
+    // little or no restoring); the rest keep their slot when possible.
+    bool relabel_tile(int L, const std::vector<int>& high, const std::vector<long>& nu, qsv_step_desc& s) {
+        std::vector<int> slots;
+        for (int p = 0; p < L; ++p)
+            slots.push_back(p);
+        for (int p : high)
+            slots.push_back(p);
+        const int ns = static_cast<int>(slots.size());
+        std::vector<int> inv(static_cast<std::size_t>(n_local), -1);
+        for (int q = 0; q < n; ++q)
+            if (pos[q] < n_local)
+                inv[pos[q]] = q;
+        std::vector<int> qs;
+        for (int p : slots)
+            qs.push_back(inv[p]);
+        auto slot_of = [&](int p) {
+            for (int i = 0; i < ns; ++i)
+                if (slots[i] == p)
+                    return i;
+            return -1;
+        };
+        std::vector<int> dest(static_cast<std::size_t>(ns), -1);   // by source slot index
+        std::vector<char> taken(static_cast<std::size_t>(ns), 0);  // by destination slot index
+        auto assign = [&](int src, int dst) {
+            dest[src] = dst;
+            taken[dst] = 1;
+        };
+        std::vector<int> order;
+        for (int i = 0; i < ns; ++i)
+            if (nu[qs[i]] < kNever)
+                order.push_back(i);
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return nu[qs[x]] < nu[qs[y]]; });
+        if (static_cast<int>(order.size()) > L)
+            order.resize(static_cast<std::size_t>(L));
+        auto is_home_of_finished = [&](int d) {
+            for (int i = 0; i < ns; ++i)
+                if (nu[qs[i]] >= kNever && qs[i] == slots[d])
+                    return true;
+            return false;
+        };
+        for (int i : order)
+            if (i < L)
+                assign(i, i);  // already low: stays
+        for (int i : order) {
+            if (dest[i] >= 0)
+                continue;
+            int pick = -1;
+            for (int d = 0; d < L && pick < 0; ++d)
+                if (!taken[d] && !is_home_of_finished(d))
+                    pick = d;
+            for (int d = 0; d < L && pick < 0; ++d)
+                if (!taken[d])
+                    pick = d;
+            assign(i, pick);
+        }
+        for (int i = 0; i < ns; ++i) {
+            if (dest[i] >= 0 || nu[qs[i]] < kNever)
+                continue;
+            const int h = qs[i] < n_local ? slot_of(qs[i]) : -1;
+            if (h >= 0 && !taken[h])
+                assign(i, h);
+        }
+        for (int i = 0; i < ns; ++i)
+            if (dest[i] < 0 && !taken[i])
+                assign(i, i);
+        for (int i = 0; i < ns; ++i) {
+            if (dest[i] >= 0)
+                continue;
+            // prefer a high slot for qubits with a later use, any free slot otherwise
+            int pick = -1;
+            for (int d = L; d < ns && pick < 0; ++d)
+                if (!taken[d])
+                    pick = d;
+            for (int d = 0; d < ns && pick < 0; ++d)
+                if (!taken[d])
+                    pick = d;
+            assign(i, pick);
+        }
+        bool moved = false;
+        for (int i = 0; i < ns; ++i) {
+            s.relabel[i] = dest[i];
+            moved |= dest[i] != i;
+        }
+        if (!moved)
+            return false;
+        s.has_relabel = 1;
+        for (int i = 0; i < ns; ++i)
+            pos[qs[i]] = slots[dest[i]];
+        return true;
+    }
+
+    int misplaced_local() const {
+        int m = 0;
+        for (int q = 0; q < n_local; ++q)
+            m += pos[q] != q;
+        return m;
+    }
+
+    // force: emit the pass even without ops (a pure relabel pass)
+    void close_pass(bool force = false) {
+        if (cur_ops.empty() && !force)
             return;
-        const int L = low_run(targets);
-        if (L < 0)
+        const bool rl = opt.relabel && seq != nullptr;
+        if (low_run(targets) < 0)
             throw std::logic_error("planner: infeasible pass tile");
+        // with relabelling the low run stays at Lmin so the high slots can carry lookahead qubits
+        const int L = rl ? Lmin : low_run(targets);
         qsv_step_desc s{};
         s.kind = QSV_STEP_PASS;
         s.tile_k = K;
@@ -734,12 +865,48 @@ struct Packer {
         for (int q : targets)
             if (q >= L)
                 high.push_back(q);
+        const int want_high = std::min(K - L, QSV_MAX_HIGH);
+        std::vector<long> nu;
+        if (rl) {
+            nu = next_use();
+            // lookahead padding: the qubits needed soonest, so the relabel can bring them low
+            std::vector<int> cand;
+            for (int q = 0; q < n; ++q)
+                if (pos[q] >= L && pos[q] < n_local && !contains(high, pos[q]) && nu[q] < kNever)
+                    cand.push_back(q);
+            std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) { return nu[x] < nu[y]; });
+            for (int q : cand)
+                if (static_cast<int>(high.size()) < want_high)
+                    high.push_back(pos[q]);
+            // restore padding: finished qubits away from home, cheapest first (a qubit
+            // whose current and home slots are both in the tile goes home this pass)
+            for (;;) {
+                int best = -1, best_cost = 3;
+                for (int q = 0; q < n_local; ++q) {
+                    if (pos[q] == q || nu[q] < kNever || pos[q] >= n_local)
+                        continue;
+                    int cost = 0;
+                    for (int p : {pos[q], q})
+                        cost += p >= L && !contains(high, p);
+                    if (cost > 0 && cost < best_cost && static_cast<int>(high.size()) + cost <= want_high) {
+                        best_cost = cost;
+                        best = q;
+                    }
+                }
+                if (best < 0)
+                    break;
+                for (int p : {pos[best], best})
+                    if (p >= L && !contains(high, p))
+                        high.push_back(p);
+            }
+        }
         // pad the tile with high qubits when targets don't fill it (K - L slots)
-        const int want_high = K - L;
         for (int q = n_local - 1; static_cast<int>(high.size()) < want_high && q >= L; --q)
             if (!contains(high, q))
                 high.push_back(q);
         std::sort(high.begin(), high.end());
+        if (rl)
+            relabels += relabel_tile(L, high, nu, s);
         s.nhigh = static_cast<int>(high.size());
         for (std::size_t i = 0; i < high.size(); ++i)
             s.high[i] = high[i];
@@ -925,52 +1092,17 @@ std::vector<int> local_needs(const Op& o) {
 
 } // namespace
 
-Plan make_plan(const Circuit& c, const PlanOptions& opt) {
-    c.validate();
-    if (opt.fuse_k < 1 || opt.fuse_k > QSV_MAX_DENSE_K)
-        throw std::invalid_argument("make_plan: fuse_k must be in [1, 5]");
-    if (opt.tile_k < 1 || opt.tile_k > 11)
-        throw std::invalid_argument("make_plan: tile_k must be in [1, 11]");
-    if (opt.rblock_k != 3 && opt.rblock_k != 4)
-        throw std::invalid_argument("make_plan: rblock_k must be 3 or 4");
-    Plan plan;
-    plan.n = c.n;
-    plan.n_local = opt.n_local < 0 ? c.n : opt.n_local;
-    if (plan.n_local < 1 || plan.n_local > c.n)
-        throw std::invalid_argument("make_plan: n_local must be in [1, n]");
-    plan.stats.gates_in = c.gate_count();
-    std::vector<Op> ops = lower(c);
-    plan.stats.ops_lowered = ops.size();
-    if (opt.fusion) {
-        ops = reduce_parity(ops);
-        PlanOptions fo = opt;
-        fo.tile_k = std::min(opt.tile_k, plan.n_local);
-        fo.min_low = std::min(opt.min_low, fo.tile_k);
-        ops = fuse_ops(ops, fo);
-    } else {
-        std::vector<Op> kept;
-        for (Op& o : ops)
-            if (o.kind != OpKind::Fence)
-                kept.push_back(std::move(o));
-        ops = std::move(kept);
-    }
-    plan.stats.ops_fused = ops.size();
-    const int K = std::min(opt.tile_k, plan.n_local);
-    if (opt.fusion && opt.register_blocks && K >= std::max(opt.min_low, 5) && opt.multi_op_passes)
-        ops = form_blocks(ops, std::min(opt.min_low, K), std::min(QSV_MAX_HIGH, K - std::min(opt.min_low, K)),
-                          opt.rblock_k);
-    plan.stats.ops_final = ops.size();
-    for (const Op& o : ops) {
-        plan.stats.cost_units += op_cost(o);
-        if (o.kind == OpKind::Dense)
-            plan.stats.max_dense_k = std::max(plan.stats.max_dense_k, static_cast<int>(o.qubits.size()));
-    }
-
+// Packs the final op list into passes (SMGP) and, across ranks, BBOP swaps.
+static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOptions& opt, Plan plan) {
     Packer pk(opt, c.n, plan.n_local, plan);
     const int nops = static_cast<int>(ops.size());
     if (plan.n_local == c.n) {
-        for (const Op& o : ops)
-            pk.add(o);
+        pk.seq = &ops;
+        for (std::size_t i = 0; i < ops.size(); ++i) {
+            pk.cursor = i;
+            pk.add(ops[i]);
+        }
+        pk.cursor = ops.size();
     } else {
         // Local-first list scheduling over the dependency DAG (multi-GPU): run
         // every ready op whose tile qubits are all local; only when none is ready
@@ -1052,6 +1184,22 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
         }
     }
     pk.close_pass();
+    if (pk.seq != nullptr && opt.relabel) {
+        // pure relabel passes until every qubit is home (each fixes the cycles it can)
+        if (std::getenv("QSV_PLAN_DEBUG"))
+            std::fprintf(stderr, "plan: before restore passes=%zu misplaced=%d\n", plan.stats.passes, pk.misplaced_local());
+        for (int guard = 0; guard < 64 && pk.misplaced_local() > 0; ++guard) {
+            const int before = pk.misplaced_local();
+            pk.close_pass(true);
+            if (pk.misplaced_local() >= before)
+                break;
+        }
+    }
+    if (std::getenv("QSV_PLAN_DEBUG")) {
+        int mis = 0;
+        for (int q = 0; q < c.n; ++q) mis += pk.pos[q] != q;
+        std::fprintf(stderr, "plan: passes=%zu relabels=%d misplaced=%d\n", plan.stats.passes, pk.relabels, mis);
+    }
     // restore the logical qubit order so the final state is in standard layout
     for (int q = 0; q < c.n; ++q) {
         if (pk.pos[q] == q)
@@ -1084,8 +1232,65 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
             pk.swap(a, t);
         }
     }
-    plan.fused = std::move(ops);
     return plan;
+}
+
+Plan make_plan(const Circuit& c, const PlanOptions& opt) {
+    c.validate();
+    if (opt.fuse_k < 1 || opt.fuse_k > QSV_MAX_DENSE_K)
+        throw std::invalid_argument("make_plan: fuse_k must be in [1, 5]");
+    if (opt.tile_k < 1 || opt.tile_k > 11)
+        throw std::invalid_argument("make_plan: tile_k must be in [1, 11]");
+    if (opt.rblock_k != 3 && opt.rblock_k != 4)
+        throw std::invalid_argument("make_plan: rblock_k must be 3 or 4");
+    Plan plan;
+    plan.n = c.n;
+    plan.n_local = opt.n_local < 0 ? c.n : opt.n_local;
+    if (plan.n_local < 1 || plan.n_local > c.n)
+        throw std::invalid_argument("make_plan: n_local must be in [1, n]");
+    plan.stats.gates_in = c.gate_count();
+    std::vector<Op> ops = lower(c);
+    plan.stats.ops_lowered = ops.size();
+    if (opt.fusion) {
+        ops = reduce_parity(ops);
+        PlanOptions fo = opt;
+        fo.tile_k = std::min(opt.tile_k, plan.n_local);
+        fo.min_low = std::min(opt.min_low, fo.tile_k);
+        ops = fuse_ops(ops, fo);
+    } else {
+        std::vector<Op> kept;
+        for (Op& o : ops)
+            if (o.kind != OpKind::Fence)
+                kept.push_back(std::move(o));
+        ops = std::move(kept);
+    }
+    plan.stats.ops_fused = ops.size();
+    const int K = std::min(opt.tile_k, plan.n_local);
+    if (opt.fusion && opt.register_blocks && K >= std::max(opt.min_low, 5) && opt.multi_op_passes)
+        ops = form_blocks(ops, std::min(opt.min_low, K), std::min(QSV_MAX_HIGH, K - std::min(opt.min_low, K)),
+                          opt.rblock_k);
+    plan.stats.ops_final = ops.size();
+    for (const Op& o : ops) {
+        plan.stats.cost_units += op_cost(o);
+        if (o.kind == OpKind::Dense)
+            plan.stats.max_dense_k = std::max(plan.stats.max_dense_k, static_cast<int>(o.qubits.size()));
+    }
+
+    // Tile relabelling is a per-circuit win or loss (lookahead saves passes, the final
+    // restore costs some): plan both ways and keep the one with fewer HBM passes.
+    if (opt.relabel < 0 || opt.relabel > 2)
+        throw std::invalid_argument("make_plan: relabel must be 0, 1 or 2");
+    PlanOptions o_plain = opt;
+    o_plain.relabel = 0;
+    const bool single = plan.n_local == c.n;
+    Plan best = (opt.relabel == 2 && single) ? pack_ops(c, ops, opt, plan) : pack_ops(c, ops, o_plain, plan);
+    if (opt.relabel == 1 && single) {
+        Plan alt = pack_ops(c, ops, opt, plan);
+        if (alt.stats.passes < best.stats.passes)
+            best = std::move(alt);
+    }
+    best.fused = std::move(ops);
+    return best;
 }
 
 Circuit ops_to_circuit(int n, const std::vector<Op>& ops) {

@@ -6,6 +6,7 @@
 #if defined(__CUDACC_RTC__)
 typedef unsigned char uint8_t;
 typedef signed char int8_t;
+typedef unsigned short uint16_t;
 typedef int int32_t;
 typedef unsigned int uint32_t;
 typedef long long int64_t;
@@ -33,6 +34,10 @@ typedef unsigned long long uint64_t;
 #define QSV_PRIM_U1R 5
 #define QSV_PRIM_U1I 6
 #endif
+
+// Internal (device-only) op kind: the pass relabel appended after a pass's ops
+// (qsv_step_desc::relabel); never appears in a qsv_op_desc.
+#define QSV_OP_RELABEL 16
 
 namespace qsv {
 

@@ -153,6 +153,9 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
                 o << "  qsv::dense_op<" << op.k << ", " << K << ", " << NT << ">(tile, " << opref << ", blob);\n";
             }
             break;
+        case QSV_OP_RELABEL:
+            o << "  qsv::relabel_op<" << K << ", " << NT << ">(tile, " << opref << ", blob);\n";
+            break;
         case QSV_OP_DIAG:
             o << "  qsv::diag_op<" << K << ", " << NT << ">(tile, " << opref << ", blob, full_base);\n";
             break;
@@ -330,53 +333,55 @@ bool jit_available(std::string& why) {
     return true;
 }
 
-int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
-    const auto t0 = std::chrono::steady_clock::now();
-    std::string why;
-    if (!jit_available(why)) {
-        set_error("qsv_program_jit: " + why);
-        return QSV_E_STATE;
-    }
-    // unique structures -> kernels
-    std::map<std::string, int> uniq;
+namespace {
+
+// Distinct pass structures of a program -> kernel sources (host only).
+struct JitPlan {
     std::vector<std::string> bodies;
     std::vector<int> kernel_k, kernel_minb;
-    prog->jit_of_step.assign(prog->steps.size(), -1);
-    for (size_t i = 0; i < prog->steps.size(); ++i) {
-        const Step& s = prog->steps[i];
+    std::vector<int> jit_of_step;
+};
+
+JitPlan plan_kernels(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels) {
+    JitPlan jp;
+    std::map<std::string, int> uniq;
+    jp.jit_of_step.assign(steps.size(), -1);
+    for (size_t i = 0; i < steps.size(); ++i) {
+        const Step& s = steps[i];
         if (s.desc.kind != QSV_STEP_PASS || s.geom.K < 4)
             continue;
         int minb = 3;
-        const std::string body = gen_ops(s, prog->host_blobs.data() + s.blob_off, minb);
+        const std::string body = gen_ops(s, host_blobs + s.blob_off, minb);
         const std::string key = std::to_string(s.geom.K) + "|" + std::to_string(minb) + "|" + body;
         auto it = uniq.find(key);
         if (it == uniq.end()) {
-            if (static_cast<int>(bodies.size()) >= max_kernels)
+            if (static_cast<int>(jp.bodies.size()) >= max_kernels)
                 continue;  // beyond the budget: this pass keeps the interpreter
-            it = uniq.emplace(key, static_cast<int>(bodies.size())).first;
-            bodies.push_back(body);
-            kernel_k.push_back(s.geom.K);
-            kernel_minb.push_back(minb);
+            it = uniq.emplace(key, static_cast<int>(jp.bodies.size())).first;
+            jp.bodies.push_back(body);
+            jp.kernel_k.push_back(s.geom.K);
+            jp.kernel_minb.push_back(minb);
         }
-        prog->jit_of_step[i] = it->second;
+        jp.jit_of_step[i] = it->second;
     }
-    const int nk = static_cast<int>(bodies.size());
-    if (nk == 0) {
-        if (seconds)
-            *seconds = 0;
-        return QSV_OK;
-    }
-    // translation units of up to 6 kernels, compiled concurrently
-    const int per_unit = 6;
-    const int nunits = (nk + per_unit - 1) / per_unit;
+    return jp;
+}
+
+constexpr int kKernelsPerUnit = 6;
+
+// NVRTC-compiles the kernels of `jp` in translation units of kKernelsPerUnit,
+// concurrently (no device needed).
+bool compile_kernels(const JitPlan& jp, std::vector<std::vector<char>>& cubins, std::string& err) {
+    const int nk = static_cast<int>(jp.bodies.size());
+    const int nunits = (nk + kKernelsPerUnit - 1) / kKernelsPerUnit;
     std::vector<std::string> srcs(nunits);
     for (int u = 0; u < nunits; ++u) {
         std::string src = kDeviceSource;
-        for (int k = u * per_unit; k < std::min(nk, (u + 1) * per_unit); ++k)
-            src += kernel_source("qsv_jit_" + std::to_string(k), kernel_k[k], kernel_minb[k], bodies[k]);
+        for (int k = u * kKernelsPerUnit; k < std::min(nk, (u + 1) * kKernelsPerUnit); ++k)
+            src += kernel_source("qsv_jit_" + std::to_string(k), jp.kernel_k[k], jp.kernel_minb[k], jp.bodies[k]);
         srcs[u] = std::move(src);
     }
-    std::vector<std::vector<char>> cubins(nunits);
+    cubins.assign(nunits, {});
     std::vector<std::string> errs(nunits);
     std::vector<char> oks(nunits, 0);
     const int nthreads = std::max(1, std::min(nunits, static_cast<int>(std::thread::hardware_concurrency())));
@@ -390,10 +395,56 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
         t.join();
     for (int u = 0; u < nunits; ++u)
         if (!oks[u]) {
-            prog->jit_of_step.assign(prog->steps.size(), -1);
-            set_error("qsv_program_jit: " + errs[u]);
-            return QSV_E_CUDA;
+            err = errs[u];
+            return false;
         }
+    return true;
+}
+
+} // namespace
+
+int jit_check(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels, int* kernels) {
+    if (!nvrtc().ok) {
+        set_error("qsv_program_jit_check: " + nvrtc().why);
+        return QSV_E_STATE;
+    }
+    const JitPlan jp = plan_kernels(steps, host_blobs, max_kernels);
+    std::vector<std::vector<char>> cubins;
+    std::string err;
+    if (!compile_kernels(jp, cubins, err)) {
+        set_error("qsv_program_jit_check: " + err);
+        return QSV_E_CUDA;
+    }
+    if (kernels)
+        *kernels = static_cast<int>(jp.bodies.size());
+    return QSV_OK;
+}
+
+int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
+    const auto t0 = std::chrono::steady_clock::now();
+    std::string why;
+    if (!jit_available(why)) {
+        set_error("qsv_program_jit: " + why);
+        return QSV_E_STATE;
+    }
+    JitPlan jp = plan_kernels(prog->steps, prog->host_blobs.data(), max_kernels);
+    prog->jit_of_step = jp.jit_of_step;
+    const int nk = static_cast<int>(jp.bodies.size());
+    if (nk == 0) {
+        if (seconds)
+            *seconds = 0;
+        return QSV_OK;
+    }
+    const int per_unit = kKernelsPerUnit;
+    const int nunits = (nk + per_unit - 1) / per_unit;
+    const std::vector<int>& kernel_k = jp.kernel_k;
+    std::vector<std::vector<char>> cubins;
+    std::string err;
+    if (!compile_kernels(jp, cubins, err)) {
+        prog->jit_of_step.assign(prog->steps.size(), -1);
+        set_error("qsv_program_jit: " + err);
+        return QSV_E_CUDA;
+    }
     // load modules and functions
     const Driver& d = driver();
     cudaSetDevice(prog->ctx->device);

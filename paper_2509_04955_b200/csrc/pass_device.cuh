@@ -160,6 +160,73 @@ __device__ __forceinline__ void dense_op(double2* tile, const TileOp& op, const 
     }
 }
 
+// Pass relabel (planner-chosen, applied after the pass's ops): tile bit b of every
+// amplitude index moves to tile bit relabel[b], an in-place permutation of the tile.
+// Thread t, iteration j handles source index x = t | j << log2(NT) mapped through an
+// XOR-linear basis built on the host (src columns at blob+mat_byte, the matching
+// destination columns 16 entries later).  The first three columns are chosen so that
+// the 8 lanes of a quarter-warp hit 8 distinct 16-B bank slots on both the gather and
+// the scatter, so the permutation costs two conflict-free SMEM sweeps.
+template <int K, int NT>
+__device__ __forceinline__ void relabel_op(double2* __restrict__ tile, const TileOp& op,
+                                           const unsigned char* blob) {
+    constexpr int TILE = 1 << K;
+    constexpr int TB = NT >= 128 ? 7 : (NT >= 64 ? 6 : 5);
+    const uint16_t* col = reinterpret_cast<const uint16_t*>(blob + op.mat_byte);
+    if constexpr (TILE >= NT) {
+        constexpr int APT = TILE / NT;
+        constexpr int IB = K - TB;
+        uint32_t sb = 0, db = 0;
+#pragma unroll
+        for (int b = 0; b < TB; ++b)
+            if ((threadIdx.x >> b) & 1u) {
+                sb ^= col[b];
+                db ^= col[16 + b];
+            }
+        uint32_t is[IB > 0 ? IB : 1], id[IB > 0 ? IB : 1];
+#pragma unroll
+        for (int b = 0; b < IB; ++b) {
+            is[b] = col[TB + b];
+            id[b] = col[16 + TB + b];
+        }
+        double2 v[APT];
+#pragma unroll
+        for (int j = 0; j < APT; ++j) {
+            uint32_t x = sb;
+#pragma unroll
+            for (int b = 0; b < IB; ++b)
+                if ((j >> b) & 1)
+                    x ^= is[b];
+            v[j] = tile[x];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < APT; ++j) {
+            uint32_t x = db;
+#pragma unroll
+            for (int b = 0; b < IB; ++b)
+                if ((j >> b) & 1)
+                    x ^= id[b];
+            tile[x] = v[j];
+        }
+    } else {
+        const bool on = threadIdx.x < TILE;
+        uint32_t sb = 0, db = 0;
+#pragma unroll
+        for (int b = 0; b < K; ++b)
+            if ((threadIdx.x >> b) & 1u) {
+                sb ^= col[b];
+                db ^= col[16 + b];
+            }
+        double2 v0 = make_double2(0.0, 0.0);
+        if (on)
+            v0 = tile[sb];
+        __syncthreads();
+        if (on)
+            tile[db] = v0;
+    }
+}
+
 template <int K, int NT>
 __device__ __forceinline__ void xperm_op(double2* tile, const TileOp& op) {
     const int nfix = op.nfix;

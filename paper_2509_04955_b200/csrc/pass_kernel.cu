@@ -75,6 +75,8 @@ pass_kernel(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, 
                 parphase_op<K, NT>(tile, op, blob, full_base);
             } else if (op.kind == QSV_OP_PHASEPROD) {
                 phaseprod_op<K, NT>(tile, op, blob, full_base);
+            } else if (op.kind == QSV_OP_RELABEL) {
+                relabel_op<K, NT>(tile, op, blob);
             } else if (op.kind == QSV_OP_DIAG) {
                 diag_op<K, NT>(tile, op, blob, full_base);
             } else {

@@ -416,6 +416,68 @@ struct BlobBuilder {
     }
 };
 
+// XOR-linear enumeration of a 2^K tile for the pass relabel (relabel_op): column c
+// is the source index contributed by bit c of x = thread | iteration << log2(NT); the
+// destination column is its image under the bit permutation rel.  Columns 0..2 (the
+// lane bits of a quarter-warp) are picked so that both the source and the destination
+// low-3 bits (the 16-B bank slot) are linearly independent, i.e. conflict-free.
+void relabel_columns(int K, const int32_t* rel, uint16_t* scol, uint16_t* dcol) {
+    auto image = [&](uint32_t v) {
+        uint32_t d = 0;
+        for (int b = 0; b < K; ++b)
+            if (v >> b & 1u)
+                d |= 1u << rel[b];
+        return d;
+    };
+    auto rank3 = [](uint32_t a, uint32_t b, uint32_t c) {  // GF(2) rank of the low-3-bit projections
+        a &= 7u;
+        b &= 7u;
+        c &= 7u;
+        return a && b && c && a != b && c != a && c != b && (a ^ b) != c;
+    };
+    std::vector<uint32_t> cols;
+    if (K >= 3) {
+        std::vector<uint32_t> cand;
+        for (int a = 0; a < K; ++a)
+            cand.push_back(1u << a);
+        for (int a = 0; a < K; ++a)
+            for (int b = a + 1; b < K; ++b)
+                cand.push_back((1u << a) | (1u << b));
+        bool found = false;
+        for (size_t i = 0; i < cand.size() && !found; ++i)
+            for (size_t j = i + 1; j < cand.size() && !found; ++j)
+                for (size_t k = j + 1; k < cand.size() && !found; ++k)
+                    if (rank3(cand[i], cand[j], cand[k]) &&
+                        rank3(image(cand[i]), image(cand[j]), image(cand[k]))) {
+                        cols = {cand[i], cand[j], cand[k]};
+                        found = true;
+                    }
+    }
+    // complete to a basis of GF(2)^K with unit vectors (pivot on the highest set bit)
+    uint32_t piv[16] = {};
+    auto insert = [&](uint32_t v) {
+        for (int b = 15; b >= 0; --b) {
+            if (!(v >> b & 1u))
+                continue;
+            if (!piv[b]) {
+                piv[b] = v;
+                return true;
+            }
+            v ^= piv[b];
+        }
+        return false;
+    };
+    for (uint32_t c : cols)
+        insert(c);
+    for (int b = 0; b < K && static_cast<int>(cols.size()) < K; ++b)
+        if (insert(1u << b))
+            cols.push_back(1u << b);
+    for (int c = 0; c < 16; ++c) {
+        scol[c] = c < K ? static_cast<uint16_t>(cols[c]) : 0;
+        dcol[c] = c < K ? static_cast<uint16_t>(image(cols[c])) : 0;
+    }
+}
+
 int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                  const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims, int nprims,
                  const double* pool, size_t pool_len, qsv::Step& step,
@@ -447,6 +509,15 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
     const uint64_t full_mask = (n_total >= 64) ? ~0ull : ((1ull << n_total) - 1ull);
     const uint64_t rank_bits = static_cast<uint64_t>(rank) << n_local;
     std::vector<TileOp> tops(d.op_count);
+    QSV_REQUIRE(d.has_relabel == 0 || d.has_relabel == 1, "pass: has_relabel must be 0 or 1");
+    if (d.has_relabel) {
+        uint32_t seen = 0;
+        for (int i = 0; i < K; ++i) {
+            const int r = d.relabel[i];
+            QSV_REQUIRE(r >= 0 && r < K && !(seen >> r & 1u), "pass: relabel must be a permutation of the tile bits");
+            seen |= 1u << r;
+        }
+    }
     struct Payload { int op; std::vector<uint32_t> off; std::vector<double> data; std::vector<uint8_t> ptab;
                      std::vector<qsv::DevPrim> dprims; std::vector<std::vector<double>> pdata; std::vector<qsv::ExtFactor> ext; };
     std::vector<Payload> payloads;
@@ -742,8 +813,19 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
         if (!pl.data.empty() || !pl.off.empty() || !pl.ptab.empty() || !pl.dprims.empty() || !pl.ext.empty())
             payloads.push_back(std::move(pl));
     }
+    std::vector<uint16_t> relabel_tab;
+    if (d.has_relabel) {
+        TileOp t{};
+        t.kind = QSV_OP_RELABEL;
+        relabel_tab.assign(32, 0);
+        relabel_columns(K, d.relabel, relabel_tab.data(), relabel_tab.data() + 16);
+        tops.push_back(t);
+        step.nops = d.op_count + 1;
+    }
     BlobBuilder bb;
     bb.append(tops.data(), tops.size() * sizeof(TileOp));
+    if (d.has_relabel)
+        tops.back().mat_byte = bb.append(relabel_tab.data(), relabel_tab.size() * sizeof(uint16_t));
     for (auto& pl : payloads) {
         TileOp& t = tops[pl.op];
         if (!pl.off.empty())
@@ -845,9 +927,13 @@ extern "C" int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local, const 
     return QSV_OK;
 }
 
-extern "C" int qsv_program_validate(int n_total, int n_local, int rank, const qsv_step_desc* steps,
-                                    int nsteps, const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims,
-                                    int nprims, const double* pool, size_t pool_len) {
+namespace {
+
+// Shared by qsv_program_validate / qsv_program_jit_check: host compile of every step.
+int compile_steps_host(int n_total, int n_local, int rank, const qsv_step_desc* steps, int nsteps,
+                       const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims, int nprims,
+                       const double* pool, size_t pool_len, std::vector<qsv::Step>* out_steps,
+                       std::vector<unsigned char>* out_blobs) {
     QSV_REQUIRE(nsteps >= 0 && (steps != nullptr || nsteps == 0), "qsv_program_validate: bad steps");
     QSV_REQUIRE(nops >= 0 && (ops != nullptr || nops == 0), "qsv_program_validate: bad ops");
     QSV_REQUIRE(n_total >= 1 && n_total <= QSV_MAX_QUBITS && n_local >= 1 && n_local <= n_total,
@@ -855,14 +941,19 @@ extern "C" int qsv_program_validate(int n_total, int n_local, int rank, const qs
     QSV_REQUIRE(rank >= 0 && (static_cast<uint64_t>(rank) >> (n_total - n_local)) == 0,
                 "qsv_program_validate: rank out of range");
     for (int i = 0; i < nsteps; ++i) {
+        qsv::Step s;
+        s.desc = steps[i];
         if (steps[i].kind == QSV_STEP_PASS) {
-            qsv::Step s;
             std::vector<unsigned char> blob;
             const int rc = compile_pass(steps[i], n_total, n_local, rank, ops, nops, prims, nprims, pool,
                                         pool_len, s, blob);
             if (rc != QSV_OK) {
                 set_error("step " + std::to_string(i) + ": " + qsv_last_error());
                 return rc;
+            }
+            if (out_blobs) {
+                s.blob_off = out_blobs->size();
+                out_blobs->insert(out_blobs->end(), blob.begin(), blob.end());
             }
         } else if (steps[i].kind == QSV_STEP_SWAP) {
             const qsv_step_desc& d = steps[i];
@@ -873,8 +964,32 @@ extern "C" int qsv_program_validate(int n_total, int n_local, int rank, const qs
         } else {
             QSV_REQUIRE(false, "step " + std::to_string(i) + ": unknown step kind");
         }
+        if (out_steps)
+            out_steps->push_back(s);
     }
     return QSV_OK;
+}
+
+} // namespace
+
+extern "C" int qsv_program_validate(int n_total, int n_local, int rank, const qsv_step_desc* steps,
+                                    int nsteps, const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims,
+                                    int nprims, const double* pool, size_t pool_len) {
+    return compile_steps_host(n_total, n_local, rank, steps, nsteps, ops, nops, prims, nprims, pool, pool_len,
+                              nullptr, nullptr);
+}
+
+extern "C" int qsv_program_jit_check(int n_total, int n_local, int rank, const qsv_step_desc* steps,
+                                     int nsteps, const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims,
+                                     int nprims, const double* pool, size_t pool_len, int max_kernels,
+                                     int* kernels) {
+    std::vector<qsv::Step> st;
+    std::vector<unsigned char> blobs;
+    const int rc = compile_steps_host(n_total, n_local, rank, steps, nsteps, ops, nops, prims, nprims, pool,
+                                      pool_len, &st, &blobs);
+    if (rc != QSV_OK)
+        return rc;
+    return qsv::jit_check(st, blobs.data(), max_kernels, kernels);
 }
 
 extern "C" int qsv_program_time(qsv_state* st, qsv_program* prog, int iters, int64_t basis, float* ms) {

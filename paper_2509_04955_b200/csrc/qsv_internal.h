@@ -99,6 +99,8 @@ cudaError_t launch_pass(const qsv_state* st, const Step& step, const unsigned ch
 // NVRTC specialisation (jit.cu).
 bool jit_available(std::string& why);
 int jit_program(qsv_program* prog, int max_kernels, double* seconds);
+// Host-only: NVRTC-compiles the distinct pass kernels of compiled steps (no device).
+int jit_check(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels, int* kernels);
 cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step, const unsigned char* d_blob,
                        uint64_t rank_base, cudaStream_t stream);
 void jit_release(qsv_program* prog);

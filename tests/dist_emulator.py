@@ -12,7 +12,8 @@ QSV_MAX_HIGH = 8
 
 class Step(C.Structure):
     _fields_ = [("kind", C.c_int32), ("tile_k", C.c_int32), ("nhigh", C.c_int32), ("high", C.c_int32 * QSV_MAX_HIGH),
-                ("op_begin", C.c_int32), ("op_count", C.c_int32), ("swap_global", C.c_int32),
+                ("op_begin", C.c_int32), ("op_count", C.c_int32), ("has_relabel", C.c_int32),
+                ("relabel", C.c_int32 * 16), ("swap_global", C.c_int32),
                 ("swap_local", C.c_int32), ("chunk_log2", C.c_int32), ("nbuf", C.c_int32)]
 
 
@@ -126,12 +127,28 @@ def apply_op(psi, op, prims, pool, rank, n_local):
         raise ValueError(f"unknown op kind {kind}")
 
 
+def relabel(psi, s, n_local):
+    """Pass relabel: tile bit i (low run, then high[] in order) moves to tile bit relabel[i]."""
+    L = s.tile_k - s.nhigh
+    slots = list(range(L)) + [s.high[i] for i in range(s.nhigh)]
+    dst_of = {slots[i]: slots[s.relabel[i]] for i in range(len(slots))}
+    # numpy axes are most-significant first: axis a <-> physical bit n_local-1-a
+    perm_src = list(range(n_local))
+    for p, d in dst_of.items():
+        perm_src[d] = p
+    view = psi.reshape((2,) * n_local)
+    out = np.transpose(view, [n_local - 1 - perm_src[n_local - 1 - a] for a in range(n_local)])
+    psi[:] = out.reshape(-1)
+
+
 def run_program(psi, steps, ops, prims, pool, rank, n_local, exchange):
     """exchange(psi, g, v, chunk_log2, nbuf) performs the swap collective."""
     for s in steps:
         if s.kind == 0:
             for op in ops[s.op_begin:s.op_begin + s.op_count]:
                 apply_op(psi, op, prims, pool, rank, n_local)
+            if s.has_relabel:
+                relabel(psi, s, n_local)
         else:
             exchange(psi, s.swap_global, s.swap_local, s.chunk_log2, s.nbuf)
     return psi
@@ -146,3 +163,28 @@ def swap_indices(n_local, rank, g, v, chunk_log2):
     idx = ((r ^ lo) << 1) | (sendbit << v) | lo
     c = 1 << chunk_log2
     return [idx[i:i + c] for i in range(0, idx.size, c)]
+
+
+def validate(steps, ops, prims, pool, n_total, n_local, rank):
+    """qsv_program_validate (host-side compile of every pass) on an exported program."""
+    L = pkg.load_qsv()
+    st = (Step * max(len(steps), 1))(*steps)
+    op = (Op * max(len(ops), 1))(*ops)
+    pr = (Prim * max(len(prims), 1))(*prims)
+    pv = np.ascontiguousarray(pool)
+    return L.qsv_program_validate(n_total, n_local, rank, st, len(steps), op, len(ops), pr, len(prims),
+                                  pv.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), C.c_size_t(pv.size))
+
+
+def jit_check(steps, ops, prims, pool, n_total, n_local, rank=0, max_kernels=512):
+    """qsv_program_jit_check: host compile + NVRTC sm_100a compile of the pass kernels."""
+    L = pkg.load_qsv()
+    st = (Step * max(len(steps), 1))(*steps)
+    op = (Op * max(len(ops), 1))(*ops)
+    pr = (Prim * max(len(prims), 1))(*prims)
+    pv = np.ascontiguousarray(pool)
+    nk = C.c_int(-1)
+    rc = L.qsv_program_jit_check(n_total, n_local, rank, st, len(steps), op, len(ops), pr, len(prims),
+                                 pv.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), C.c_size_t(pv.size),
+                                 max_kernels, C.byref(nk))
+    return rc, nk.value

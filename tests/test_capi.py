@@ -54,7 +54,8 @@ def test_program_validate_rejects_bad_programs():
 
     class Step(C.Structure):
         _fields_ = [("kind", C.c_int32), ("tile_k", C.c_int32), ("nhigh", C.c_int32), ("high", C.c_int32 * 8),
-                    ("op_begin", C.c_int32), ("op_count", C.c_int32), ("swap_global", C.c_int32),
+                    ("op_begin", C.c_int32), ("op_count", C.c_int32), ("has_relabel", C.c_int32),
+                ("relabel", C.c_int32 * 16), ("swap_global", C.c_int32),
                     ("swap_local", C.c_int32), ("chunk_log2", C.c_int32), ("nbuf", C.c_int32)]
 
     class Op(C.Structure):

@@ -41,6 +41,9 @@ OPTS = {
     "tile8": pkg.PlanOptions(tile_k=8, pass_budget=200),
     "rblock4": pkg.PlanOptions(rblock_k=4, tile_k=11),
     "tile11": pkg.PlanOptions(tile_k=11),
+    "relabel": pkg.PlanOptions(relabel=2),
+    "relabel-t8": pkg.PlanOptions(relabel=2, tile_k=8, min_low=4),
+    "relabel-interp": pkg.PlanOptions(relabel=2, tile_k=7, min_low=3, jit=False),
 }
 
 
@@ -141,11 +144,12 @@ def test_qft24_random_state_vs_oracle():  # BASELINE configs[0]: same circuit, C
     assert abs(norm - 1) <= NORM_TOL
 
 
+@pytest.mark.parametrize("relabel", [0, 2])
 @pytest.mark.parametrize("spec", ["random:22:20:2", "hea:22:5:4", "uccsd:20:3000:3"])
-def test_config_shapes_at_reduced_size(spec):  # configs[1..3] shapes, oracle-checkable sizes
+def test_config_shapes_at_reduced_size(spec, relabel):  # configs[1..3] shapes, oracle-checkable sizes
     c = pkg.Circuit.generate(spec)
     ref = O.run_local(c)
-    for o in (pkg.PlanOptions(), pkg.PlanOptions(fusion=False)):
+    for o in (pkg.PlanOptions(relabel=relabel), pkg.PlanOptions(fusion=False, relabel=relabel)):
         got, norm = run_gpu(c, None, o)
         assert np.abs(got - ref).max() <= TOL
         assert abs(norm - 1) <= NORM_TOL
