@@ -857,7 +857,7 @@ struct Packer {
         if (low_run(targets) < 0)
             throw std::logic_error("planner: infeasible pass tile");
         // with relabelling the low run stays at Lmin so the high slots can carry lookahead qubits
-        const int L = rl ? Lmin : low_run(targets);
+        const int L = (rl || std::getenv("QSV_PLAN_FIXED_L")) ? Lmin : low_run(targets);
         qsv_step_desc s{};
         s.kind = QSV_STEP_PASS;
         s.tile_k = K;
@@ -1092,6 +1092,26 @@ std::vector<int> local_needs(const Op& o) {
 
 } // namespace
 
+// Relative time of a plan in units of one HBM round trip, from the B200
+// measurements in profiles/ (r01): a relabel costs an extra SMEM sweep (~17 % of
+// a pass) and runs shorter than 1 KB lose DRAM efficiency (~16 % at 512 B).
+static double plan_time_model(const Plan& p) {
+    double t = 0;
+    for (const qsv_step_desc& s : p.steps) {
+        if (s.kind != QSV_STEP_PASS) {
+            t += 1.0;
+            continue;
+        }
+        const int L = s.tile_k - s.nhigh;
+        int m = 0;
+        while (m < s.nhigh && s.high[m] == L + m)
+            ++m;
+        const int run = L + m;
+        t += 1.0 + (s.has_relabel ? 0.17 : 0.0) + (run <= 5 ? 0.16 : (run == 6 ? 0.05 : 0.0));
+    }
+    return t;
+}
+
 // Packs the final op list into passes (SMGP) and, across ranks, BBOP swaps.
 static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOptions& opt, Plan plan) {
     Packer pk(opt, c.n, plan.n_local, plan);
@@ -1285,9 +1305,16 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     const bool single = plan.n_local == c.n;
     Plan best = (opt.relabel == 2 && single) ? pack_ops(c, ops, opt, plan) : pack_ops(c, ops, o_plain, plan);
     if (opt.relabel == 1 && single) {
-        Plan alt = pack_ops(c, ops, opt, plan);
-        if (alt.stats.passes < best.stats.passes)
-            best = std::move(alt);
+        // relabelled plans keep >= 1 KB HBM runs (min_low 6): 512-B runs cost ~16 %
+        PlanOptions o_rl = opt;
+        o_rl.min_low = std::max(opt.min_low, 6);
+        try {
+            Plan alt = pack_ops(c, ops, o_rl, plan);
+            if (plan_time_model(alt) < plan_time_model(best))
+                best = std::move(alt);
+        } catch (const std::logic_error&) {
+            // the blocks were formed for the caller's low run; a longer one may not fit
+        }
     }
     best.fused = std::move(ops);
     return best;

@@ -169,6 +169,61 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
             o << "  qsv::xperm_op<" << K << ", " << NT << ">(tile, " << opref << ");\n";
             break;
         case QSV_OP_RBLOCK: {
+            // Diagonal ops right after a whole-tile register block ride along as a
+            // per-amplitude epilogue: no extra SMEM sweep or barrier for them.
+            std::ostringstream pre, epi;
+            int last = i;
+            if (op.xctrl == 0 && op.tctrl == 0 && !std::getenv("QSV_JIT_NO_EPI")) {
+                for (int j = i + 1; j < s.nops; ++j) {
+                    const TileOp& d = ops[j];
+                    if (d.kind != QSV_OP_DIAG && d.kind != QSV_OP_PHASEPROD && d.kind != QSV_OP_PARPHASE)
+                        break;
+                    const std::string dref = "(*reinterpret_cast<const qsv::TileOp*>(blob + " +
+                                             std::to_string(j * sizeof(TileOp)) + "))";
+                    const std::string J = std::to_string(j);
+                    std::string guard;
+                    if (d.xctrl) {
+                        pre << "  const bool on" << J << " = (full_base & " << u64(d.xctrl) << ") == " << u64(d.xctrl) << ";\n";
+                        guard = "on" + J;
+                    }
+                    if (d.tctrl) {
+                        if (!guard.empty())
+                            guard += " && ";
+                        guard += "((idx & " + u32(d.tctrl) + ") == " + u32(d.tctrl) + ")";
+                    }
+                    std::string stmt;
+                    if (d.kind == QSV_OP_DIAG) {
+                        const std::string Dg = "reinterpret_cast<const double2*>(blob + " + std::to_string(d.mat_byte) + ")";
+                        pre << "  const uint32_t e" << J << " = qsv::diag_ext(" << dref << ", full_base);\n";
+                        if (d.nin == 0) {
+                            pre << "  const double2 d" << J << " = " << Dg << "[e" << J << "];\n";
+                            stmt = "a = qsv::cmul(d" + J + ", a);";
+                        } else if (d.nin == 1) {
+                            int pbit = 0;
+                            while (!((d.tmask >> pbit) & 1u))
+                                ++pbit;
+                            pre << "  const double2 d" << J << "a = " << Dg << "[e" << J << "], d" << J << "b = " << Dg
+                                << "[e" << J << " | 1u];\n";
+                            stmt = "a = qsv::cmul(((idx >> " + std::to_string(pbit) + ") & 1u) ? d" + J + "b : d" + J + "a, a);";
+                        } else {
+                            const std::string plo = "(blob + " + std::to_string(d.ptab_byte) + ")";
+                            stmt = "a = qsv::cmul(" + Dg + "[e" + J + " | " + plo + "[idx & 31u] | " + plo +
+                                   "[32u + (idx >> 5)]], a);";
+                        }
+                    } else if (d.kind == QSV_OP_PHASEPROD) {
+                        const std::string tab = "reinterpret_cast<const double2*>(blob + " + std::to_string(d.mat_byte) + ")";
+                        pre << "  const double2 c" << J << " = qsv::pp_const(" << dref << ", blob, full_base);\n";
+                        stmt = "a = qsv::cmul(qsv::cmul(c" + J + ", qsv::cmul(" + tab + "[1u + (idx & 31u)], " + tab +
+                               "[33u + (idx >> 5)])), a);";
+                    } else {
+                        pre << "  double2 p" << J << "a, p" << J << "b;\n  qsv::par_consts(" << dref
+                            << ", blob, full_base, p" << J << "a, p" << J << "b);\n";
+                        stmt = "a = qsv::cmul((__popc(idx & " + u32(d.tmask) + ") & 1) ? p" + J + "b : p" + J + "a, a);";
+                    }
+                    epi << "    " << (guard.empty() ? "" : "if (" + guard + ") ") << stmt << "\n";
+                    last = j;
+                }
+            }
             const int KB = op.k;
             const int NV = 1 << KB;
             uint32_t m[4] = {0, 0, 0, 0};
@@ -180,6 +235,14 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
             o << "  qsv::jit_rblock<" << K << ", " << NT << ", " << KB << ", " << u32(op.fmask) << ", "
               << u32(op.tctrl) << ", " << u32(m[0]) << ", " << u32(m[1]) << ", " << u32(m[2]) << ", " << u32(m[3])
               << ", " << u32(op.rot_tab) << ">(tile, [&](double2 (&v)[" << NV << "], uint32_t r) {\n";
+            if (last > i) {
+                // hoisted constants must precede the call: re-emit the call after them
+                std::string call = o.str();
+                const std::string head = "  qsv::jit_rblock<";
+                const size_t at = call.rfind(head);
+                o.str("");
+                o << call.substr(0, at) << pre.str() << call.substr(at);
+            }
             o << "    (void)r;\n";
             const DevPrim* pr = reinterpret_cast<const DevPrim*>(blob + op.prim_byte);
             for (int p = 0; p < op.nprim; ++p) {
@@ -214,7 +277,12 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
                     break;
                 }
             }
-            o << "  });\n";
+            if (last > i) {
+                o << "  }, [&](double2& a, uint32_t idx) {\n    (void)idx;\n" << epi.str() << "  });\n";
+                i = last;  // the fused diagonal ops are done
+            } else {
+                o << "  });\n";
+            }
             break;
         }
         default:
@@ -227,13 +295,26 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
     return o.str();
 }
 
+// Tile buffers / prefetch distance of the specialised kernels (QSV_TILE_NBUF,
+// QSV_TILE_PD override the defaults for experiments).
+int env_int(const char* name, int dflt, int lo, int hi) {
+    const char* v = std::getenv(name);
+    if (!v)
+        return dflt;
+    const int x = std::atoi(v);
+    return x < lo ? lo : (x > hi ? hi : x);
+}
+int tile_nbuf() { return env_int("QSV_TILE_NBUF", kNumBuf, 2, 4); }
+int tile_pd() { return env_int("QSV_TILE_PD", tile_nbuf() - 1, 1, tile_nbuf() - 1); }
+
 std::string kernel_source(const std::string& name, int K, int minb, const std::string& body) {
     std::ostringstream o;
     const int NT = threads_for_k(K);
     o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb << ") " << name
       << "(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, uint32_t blob_bytes,\n"
       << "    const __grid_constant__ qsv::GeomArg geom, uint64_t rank_base, uint64_t ntiles) {\n"
-      << "  qsv::pass_pipeline<" << K << ", " << NT << ">(psi, gblob, blob_bytes, geom, rank_base, ntiles,\n"
+      << "  qsv::pass_pipeline<" << K << ", " << NT << ", " << tile_nbuf() << ", " << tile_pd()
+      << ">(psi, gblob, blob_bytes, geom, rank_base, ntiles,\n"
       << "    [&](double2* tile, const unsigned char* blob, uint64_t full_base) {\n"
       << "  (void)full_base;\n"
       << body << "  });\n}\n";
@@ -272,6 +353,11 @@ void mkdirs(const std::string& p) {
 
 // Compiles one translation unit to a cubin (or loads it from the cache).
 bool compile_unit(const std::string& src, std::vector<char>& cubin, std::string& err) {
+    if (const char* dump = std::getenv("QSV_JIT_DUMP")) {  // debugging: keep the generated source
+        char name[64];
+        std::snprintf(name, sizeof(name), "/qsv_%016llx.cu", static_cast<unsigned long long>(fnv1a(src)));
+        std::ofstream(std::string(dump) + name) << src;
+    }
     static const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-diag-suppress=177,550"};
     std::string key = src;
     for (const char* op : opts)
@@ -467,7 +553,7 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
                 return QSV_E_CUDA;
             }
             const int K = kernel_k[k];
-            const size_t tile_smem = sizeof(double2) * kNumBuf * (size_t{1} << K);
+            const size_t tile_smem = sizeof(double2) * tile_nbuf() * (size_t{1} << K);
             d.set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                        static_cast<int>(tile_smem + kMaxBlobBytes));
             prog->jit_kernels[k].func = f;

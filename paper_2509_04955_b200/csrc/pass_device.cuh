@@ -55,6 +55,12 @@ __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+// Wait until at most N of this thread's bulk groups are still reading SMEM.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void fence_proxy_async() {
@@ -571,6 +577,35 @@ __device__ __forceinline__ void parphase_op(double2* tile, const TileOp& op, con
     }
 }
 
+// ------------------------------------------------ diagonal epilogue constants
+// Per-tile (CTA-uniform) parts of the diagonal ops the JIT folds into the
+// preceding register block (the per-amplitude parts are generated inline with
+// the same arithmetic as diag_op / phaseprod_op / parphase_op).
+__device__ __forceinline__ uint32_t diag_ext(const TileOp& op, uint64_t full_base) {
+    uint32_t e0 = 0;
+    for (int j = op.nin; j < op.k; ++j)
+        e0 |= static_cast<uint32_t>((full_base >> op.xbit[j - op.nin]) & 1ull) << j;
+    return e0;
+}
+
+__device__ __forceinline__ void par_consts(const TileOp& op, const unsigned char* blob, uint64_t full_base,
+                                           double2& p0, double2& p1) {
+    const double2* P = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    const uint32_t ext = static_cast<uint32_t>(__popcll(full_base & op.xmask)) & 1u;
+    p0 = P[ext];
+    p1 = P[ext ^ 1u];
+}
+
+__device__ __forceinline__ double2 pp_const(const TileOp& op, const unsigned char* blob, uint64_t full_base) {
+    const double2* tab = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    const ExtFactor* ext = reinterpret_cast<const ExtFactor*>(blob + op.prim_byte);
+    double2 c = tab[0];
+    for (int i = 0; i < op.nprim; ++i)
+        if ((full_base >> ext[i].bit) & 1ull)
+            c = cmul(c, make_double2(ext[i].re, ext[i].im));
+    return c;
+}
+
 // ---------------------------------------------------------------- PHASEPROD
 // amp *= c * prod_{q in Q, bit q set} f_q for amplitudes with the controls set.
 // In-tile factors are pre-tabulated over the low 5 tile bits (A[32]) and the
@@ -616,20 +651,32 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const GeomArg& g) {
 
 // The persistent TMA pipeline of a pass; `ops(tile, blob, full_base)` applies
 // the pass's ops to one SMEM-resident tile (interpreted or JIT-specialised).
-template <int K, int NT, typename Ops>
+// NBUF tile buffers, loads issued PD tiles ahead: the load of tile t + PD reuses
+// the buffer of tile t + PD - NBUF, whose store was committed NBUF - PD - 1
+// iterations before the current one, so warp 0 only waits for stores older than
+// that (NBUF = 2, PD = 1: the previous tile's store must have left SMEM).
+template <int K, int NT, int NBUF = kNumBuf, int PD = NBUF - 1, typename Ops>
 __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const unsigned char* __restrict__ gblob,
                                               uint32_t blob_bytes, const GeomArg& geom, uint64_t rank_base,
                                               uint64_t ntiles, Ops&& ops) {
     constexpr int TILE = 1 << K;
     extern __shared__ __align__(128) unsigned char smem[];
     double2* bufs = reinterpret_cast<double2*>(smem);
-    unsigned char* blob = smem + sizeof(double2) * kNumBuf * TILE;
+    static_assert(PD >= 1 && PD < NBUF, "prefetch distance must be in [1, NBUF)");
+    unsigned char* blob = smem + sizeof(double2) * NBUF * TILE;
     __shared__ uint64_t hi_off[1 << QSV_MAX_HIGH];
-    __shared__ __align__(8) uint64_t mbar[kNumBuf];
+    __shared__ __align__(8) uint64_t mbar[NBUF];
 
     const int nh = 1 << geom.nhigh;
     const int L = geom.L;
-    const uint32_t run_bytes = static_cast<uint32_t>(sizeof(double2)) << L;
+    // High qubits that continue the low run (high[i] == L + i) are contiguous in
+    // HBM too: merge them into the bulk copies (fewer, longer TMA runs).
+    int m = 0;
+    while (m < geom.nhigh && geom.high[m] == L + m)
+        ++m;
+    const int RL = L + m;
+    const int nruns = nh >> m;
+    const uint32_t run_bytes = static_cast<uint32_t>(sizeof(double2)) << RL;
     for (int j = threadIdx.x; j < nh; j += NT) {
         uint64_t o = 0;
         for (int i = 0; i < geom.nhigh; ++i)
@@ -643,7 +690,7 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
             dst[i] = __ldg(src + i);
     }
     if (threadIdx.x == 0) {
-        for (int b = 0; b < kNumBuf; ++b)
+        for (int b = 0; b < NBUF; ++b)
             mbar_init(&mbar[b], 1);
         fence_mbar_init();
     }
@@ -659,12 +706,12 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         if (lane == 0)
             mbar_expect_tx(&mbar[b], static_cast<uint32_t>(sizeof(double2) * TILE));
         __syncwarp();
-        for (int j = lane; j < nh; j += 32)
-            bulk_load(dst + (j << L), psi + base + hi_off[j], run_bytes, &mbar[b]);
+        for (int j = lane; j < nruns; j += 32)
+            bulk_load(dst + (j << RL), psi + base + hi_off[j << m], run_bytes, &mbar[b]);
     };
 
     if (threadIdx.x < 32) {
-        for (int s = 0; s < kNumBuf - 1; ++s) {
+        for (int s = 0; s < PD; ++s) {
             const uint64_t t = blockIdx.x + s * stride;
             if (t < ntiles)
                 issue_load(t, s);
@@ -673,18 +720,18 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
 
     int it = 0;
     for (uint64_t t = blockIdx.x; t < ntiles; t += stride, ++it) {
-        const int b = it % kNumBuf;
+        const int b = it % NBUF;
         if (threadIdx.x < 32) {
-            const uint64_t tn = t + (kNumBuf - 1) * stride;
+            const uint64_t tn = t + PD * stride;
             if (tn < ntiles) {
-                // Buffer (it + NBUF - 1) % NBUF was last stored from in iteration
-                // it - 1: every lane waits for its own store groups to finish reading.
-                bulk_wait_read_all();
+                // Buffer (it + PD) % NBUF was last stored from in iteration
+                // it + PD - NBUF: every lane waits for its own store groups that old.
+                bulk_wait_read<NBUF - PD - 1>();
                 __syncwarp();
-                issue_load(tn, (it + kNumBuf - 1) % kNumBuf);
+                issue_load(tn, (it + PD) % NBUF);
             }
         }
-        mbar_wait(&mbar[b], static_cast<uint32_t>((it / kNumBuf) & 1));
+        mbar_wait(&mbar[b], static_cast<uint32_t>((it / NBUF) & 1));
         double2* tile = bufs + b * TILE;
         const uint64_t base = tile_base(t, geom);
         const uint64_t full_base = rank_base | base;
@@ -695,8 +742,8 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         fence_proxy_async();
         __syncthreads();
         if (threadIdx.x < 32) {
-            for (int j = lane; j < nh; j += 32)
-                bulk_store(psi + base + hi_off[j], tile + (j << L), run_bytes);
+            for (int j = lane; j < nruns; j += 32)
+                bulk_store(psi + base + hi_off[j << m], tile + (j << RL), run_bytes);
             bulk_commit();
         }
     }
@@ -737,9 +784,15 @@ __device__ __forceinline__ void rb_cx_plain(double2 (&v)[NV]) {
 
 // Register block with every structural quantity a compile-time constant; the
 // generated `body(v, r)` is the block's primitive sequence as straight-line code.
+struct NoEpi {
+    __device__ __forceinline__ void operator()(double2&, uint32_t) const {}
+};
+
+// `epi(v, idx)` (JIT diagonal epilogue) runs on every amplitude before it is
+// written back; only used when the block covers the whole tile (TCTRL == 0).
 template <int K, int NT, int KB, uint32_t F, uint32_t TCTRL, uint32_t M0, uint32_t M1, uint32_t M2, uint32_t M3,
-          uint32_t ROT, typename Body>
-__device__ __forceinline__ void jit_rblock(double2* tile, Body&& body) {
+          uint32_t ROT, typename Body, typename Epi = NoEpi>
+__device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi = Epi{}) {
     constexpr int NV = 1 << KB;
     constexpr uint32_t groups = 1u << (K - cpopc(F));
     constexpr uint32_t dstep = cdeposit(NT, F);
@@ -758,8 +811,11 @@ __device__ __forceinline__ void jit_rblock(double2* tile, Body&& body) {
             v[j] = tile[base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))];
         body(v, r);
 #pragma unroll
-        for (int j = 0; j < NV; ++j)
-            tile[base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))] = v[j];
+        for (int j = 0; j < NV; ++j) {
+            const uint32_t idx = base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u));
+            epi(v[j], idx);
+            tile[idx] = v[j];
+        }
         b = ((b | F) + dstep) & ~F;
     }
 }

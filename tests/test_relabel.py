@@ -35,8 +35,12 @@ def test_relabel_used_and_saves_passes():
         c, on, off = _plans(spec)
         steps, *_ = E.export_plan(c, on, c.n)
         used += sum(s.has_relabel for s in steps)
-        auto = pkg.PlanOptions(relabel=1, tile_k=7, min_low=3)
-        assert c.plan(auto)["passes"] == min(c.plan(on)["passes"], c.plan(off)["passes"])
+        auto = c.plan(pkg.PlanOptions(relabel=1, tile_k=7, min_low=3))["passes"]
+        try:
+            on6 = c.plan(pkg.PlanOptions(relabel=2, tile_k=7, min_low=6))["passes"]
+        except pkg.QsvError:
+            on6 = None  # blocks do not fit the longer low run: auto keeps the plain plan
+        assert auto in (on6, c.plan(off)["passes"])  # auto: the cheaper of the two by the time model
     assert used > 0
 
 
