@@ -102,6 +102,8 @@ void* qsim_engine_qsv_program(qsim_engine* e); /* qsv_program* */
 int qsim_engine_set_basis(qsim_engine* e, uint64_t global_index);
 int qsim_engine_upload(qsim_engine* e, const double* amps, uint64_t offset, uint64_t count);
 int qsim_engine_download(qsim_engine* e, double* amps, uint64_t offset, uint64_t count);
+/* Stream-ordered (returns before the copy completes; qsim_engine_sync waits). */
+int qsim_engine_download_async(qsim_engine* e, double* amps, uint64_t offset, uint64_t count);
 int qsim_engine_run(qsim_engine* e);           /* enqueue (asynchronous) */
 int qsim_engine_sync(qsim_engine* e);
 int qsim_engine_time(qsim_engine* e, int iters, int64_t basis, float* ms);

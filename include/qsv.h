@@ -92,6 +92,10 @@ int qsv_state_set_basis(qsv_state* st, uint64_t global_index);
  * (qsv_host_alloc) for asynchronous overlap. */
 int qsv_state_upload(qsv_state* st, const double* host, uint64_t offset, uint64_t count);
 int qsv_state_download(qsv_state* st, double* host, uint64_t offset, uint64_t count);
+/* Stream-ordered download (no host sync): the copy completes in order with the
+ * context stream; call qsv_sync before reading `host`.  With pinned host memory it
+ * overlaps other contexts' work (used for pipelined end-to-end streaming). */
+int qsv_state_download_async(qsv_state* st, double* host, uint64_t offset, uint64_t count);
 /* Raw device pointer of the shard (double2*), for interop/tests. */
 int qsv_state_device_ptr(qsv_state* st, void** ptr);
 /* Pinned host buffers for the upload/download paths. */

@@ -382,6 +382,14 @@ int qsim_engine_download(qsim_engine* e, double* amps, uint64_t offset, uint64_t
     });
 }
 
+int qsim_engine_download_async(qsim_engine* e, double* amps, uint64_t offset, uint64_t count) {
+    return guard([&] {
+        REQUIRE(e, "qsim_engine_download_async: null engine");
+        qsim::qsv_check(qsv_state_download_async(e->st->get(), amps, offset, count), "qsv_state_download_async");
+        return QSV_OK;
+    });
+}
+
 int qsim_engine_run(qsim_engine* e) {
     return guard([&] {
         REQUIRE(e, "qsim_engine_run: null engine");

@@ -1070,7 +1070,8 @@ struct Packer {
         s.kind = QSV_STEP_SWAP;
         s.swap_global = g_phys;
         s.swap_local = v_phys;
-        s.chunk_log2 = std::min(opt.chunk_log2, n_local - 1);
+        // >= 4 chunks per swap so region passes can overlap the transfer (BBOP)
+        s.chunk_log2 = std::max(0, std::min(opt.chunk_log2, n_local - 3));
         s.nbuf = opt.nbuf;
         plan.steps.push_back(s);
         plan.stats.swaps++;

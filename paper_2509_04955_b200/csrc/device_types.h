@@ -89,6 +89,7 @@ struct ExtFactor {
 struct GeomArg {
     int32_t L, nhigh;
     int32_t high[QSV_MAX_HIGH];
+    uint64_t tile0;  // first tile of the launch (region launches overlapped with a swap)
 };
 
 // Largest per-pass blob (bytes of shared memory on top of the tile buffers).

@@ -570,7 +570,7 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
 }
 
 cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step, const unsigned char* d_blob,
-                       uint64_t rank_base, cudaStream_t stream) {
+                       uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg) {
     const Step& s = prog->steps[step];
     const JitKernel& jk = prog->jit_kernels[prog->jit_of_step[step]];
     const size_t smem = jk.tile_smem + s.blob_bytes;
@@ -583,8 +583,13 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
     ga.nhigh = s.geom.nhigh;
     for (int i = 0; i < s.geom.nhigh; ++i)
         ga.high[i] = s.geom.high[i];
-    const uint64_t tiles = st->size >> s.geom.K;
-    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * st->ctx->sm_count);
+    const uint64_t all_tiles = st->size >> s.geom.K;
+    ga.tile0 = std::min(rg.tile0, all_tiles);
+    const uint64_t tiles = std::min(rg.count, all_tiles - ga.tile0);
+    if (tiles == 0)
+        return cudaSuccess;
+    const int sms = rg.sms > 0 ? std::min(rg.sms, st->ctx->sm_count) : st->ctx->sm_count;
+    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * sms);
     double2* psi = st->amps;
     uint32_t bb = s.blob_bytes;
     uint64_t rb = rank_base, nt = tiles;

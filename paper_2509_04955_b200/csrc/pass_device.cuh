@@ -701,7 +701,7 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     // byte count, then the 32 lanes issue the 2^nhigh run copies between them.
     const int lane = threadIdx.x & 31;
     auto issue_load = [&](uint64_t t, int b) {
-        const uint64_t base = tile_base(t, geom);
+        const uint64_t base = tile_base(geom.tile0 + t, geom);
         double2* dst = bufs + b * TILE;
         if (lane == 0)
             mbar_expect_tx(&mbar[b], static_cast<uint32_t>(sizeof(double2) * TILE));
@@ -733,7 +733,7 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         }
         mbar_wait(&mbar[b], static_cast<uint32_t>((it / NBUF) & 1));
         double2* tile = bufs + b * TILE;
-        const uint64_t base = tile_base(t, geom);
+        const uint64_t base = tile_base(geom.tile0 + t, geom);
         const uint64_t full_base = rank_base | base;
 
         ops(tile, blob, full_base);

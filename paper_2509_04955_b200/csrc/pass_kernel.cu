@@ -93,7 +93,7 @@ constexpr int threads_for() {
 
 template <int K, int KMAX>
 cudaError_t launch_variant(const qsv_state* st, const Step& step, const unsigned char* d_blob,
-                           uint64_t rank_base, cudaStream_t stream) {
+                           uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg) {
     constexpr int NT = threads_for<K>();
     constexpr size_t tile_smem = sizeof(double2) * kNumBuf * (size_t{1} << K);
     const size_t smem = tile_smem + step.blob_bytes;
@@ -121,8 +121,13 @@ cudaError_t launch_variant(const qsv_state* st, const Step& step, const unsigned
     ga.nhigh = step.geom.nhigh;
     for (int i = 0; i < step.geom.nhigh; ++i)
         ga.high[i] = step.geom.high[i];
-    const uint64_t tiles = st->size >> K;
-    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * sm_count);
+    const uint64_t all_tiles = st->size >> K;
+    ga.tile0 = std::min(rg.tile0, all_tiles);
+    const uint64_t tiles = std::min(rg.count, all_tiles - ga.tile0);
+    if (tiles == 0)
+        return cudaSuccess;
+    const int sms = rg.sms > 0 ? std::min(rg.sms, sm_count) : sm_count;
+    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * sms);
     kern<<<static_cast<unsigned>(grid), NT, smem, stream>>>(st->amps, d_blob, step.blob_bytes,
                                                            step.nops, ga, rank_base, tiles);
     return cudaGetLastError();
@@ -130,37 +135,37 @@ cudaError_t launch_variant(const qsv_state* st, const Step& step, const unsigned
 
 template <int K>
 cudaError_t launch_k(const qsv_state* st, const Step& step, const unsigned char* d_blob,
-                     uint64_t rank_base, cudaStream_t stream) {
+                     uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg) {
     if constexpr (K >= 9) {
         switch (step.geom.kmax <= 1 ? 1 : step.geom.kmax) {
-        case 1: return launch_variant<K, 1>(st, step, d_blob, rank_base, stream);
-        case 2: return launch_variant<K, 2>(st, step, d_blob, rank_base, stream);
-        case 3: return launch_variant<K, 3>(st, step, d_blob, rank_base, stream);
-        case 4: return launch_variant<K, 4>(st, step, d_blob, rank_base, stream);
-        default: return launch_variant<K, 5>(st, step, d_blob, rank_base, stream);
+        case 1: return launch_variant<K, 1>(st, step, d_blob, rank_base, stream, rg);
+        case 2: return launch_variant<K, 2>(st, step, d_blob, rank_base, stream, rg);
+        case 3: return launch_variant<K, 3>(st, step, d_blob, rank_base, stream, rg);
+        case 4: return launch_variant<K, 4>(st, step, d_blob, rank_base, stream, rg);
+        default: return launch_variant<K, 5>(st, step, d_blob, rank_base, stream, rg);
         }
     } else {
         constexpr int KM = K < 5 ? K : 5;
-        return launch_variant<K, KM>(st, step, d_blob, rank_base, stream);
+        return launch_variant<K, KM>(st, step, d_blob, rank_base, stream, rg);
     }
 }
 
 } // namespace
 
 cudaError_t launch_pass(const qsv_state* st, const Step& step, const unsigned char* d_blob,
-                        uint64_t rank_base, cudaStream_t stream) {
+                        uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg) {
     switch (step.geom.K) {
-    case 1: return launch_k<1>(st, step, d_blob, rank_base, stream);
-    case 2: return launch_k<2>(st, step, d_blob, rank_base, stream);
-    case 3: return launch_k<3>(st, step, d_blob, rank_base, stream);
-    case 4: return launch_k<4>(st, step, d_blob, rank_base, stream);
-    case 5: return launch_k<5>(st, step, d_blob, rank_base, stream);
-    case 6: return launch_k<6>(st, step, d_blob, rank_base, stream);
-    case 7: return launch_k<7>(st, step, d_blob, rank_base, stream);
-    case 8: return launch_k<8>(st, step, d_blob, rank_base, stream);
-    case 9: return launch_k<9>(st, step, d_blob, rank_base, stream);
-    case 10: return launch_k<10>(st, step, d_blob, rank_base, stream);
-    case 11: return launch_k<11>(st, step, d_blob, rank_base, stream);
+    case 1: return launch_k<1>(st, step, d_blob, rank_base, stream, rg);
+    case 2: return launch_k<2>(st, step, d_blob, rank_base, stream, rg);
+    case 3: return launch_k<3>(st, step, d_blob, rank_base, stream, rg);
+    case 4: return launch_k<4>(st, step, d_blob, rank_base, stream, rg);
+    case 5: return launch_k<5>(st, step, d_blob, rank_base, stream, rg);
+    case 6: return launch_k<6>(st, step, d_blob, rank_base, stream, rg);
+    case 7: return launch_k<7>(st, step, d_blob, rank_base, stream, rg);
+    case 8: return launch_k<8>(st, step, d_blob, rank_base, stream, rg);
+    case 9: return launch_k<9>(st, step, d_blob, rank_base, stream, rg);
+    case 10: return launch_k<10>(st, step, d_blob, rank_base, stream, rg);
+    case 11: return launch_k<11>(st, step, d_blob, rank_base, stream, rg);
     default: return cudaErrorInvalidValue;
     }
 }

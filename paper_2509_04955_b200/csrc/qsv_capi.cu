@@ -385,6 +385,15 @@ extern "C" int qsv_state_download(qsv_state* st, double* host, uint64_t offset, 
     return QSV_OK;
 }
 
+extern "C" int qsv_state_download_async(qsv_state* st, double* host, uint64_t offset, uint64_t count) {
+    QSV_REQUIRE(st != nullptr && (host != nullptr || count == 0), "qsv_state_download_async: null argument");
+    QSV_REQUIRE(offset <= st->size && count <= st->size - offset, "qsv_state_download_async: range outside shard");
+    QSV_CUDA(cudaSetDevice(st->ctx->device));
+    QSV_CUDA(cudaMemcpyAsync(host, st->amps + offset, count * sizeof(double2), cudaMemcpyDeviceToHost,
+                             st->ctx->stream));
+    return QSV_OK;
+}
+
 extern "C" int qsv_state_device_ptr(qsv_state* st, void** ptr) {
     QSV_REQUIRE(st != nullptr && ptr != nullptr, "qsv_state_device_ptr: null argument");
     *ptr = st->amps;
@@ -1052,19 +1061,94 @@ extern "C" int qsv_program_jit_info(qsv_program* prog, int* kernels, int* steps_
 
 namespace {
 
+// BBOP overlap: can pass `p` run region by region behind swap (v, b)?  Region c of
+// a swap = the shard slice whose half-index (index with bit v removed) has top
+// bits c; a pass qualifies when none of its tile qubits is a region bit, so its
+// tiles split into contiguous per-region ranges (region bits = top non-tile bits).
+bool region_pass_ok(const qsv::Step& p, int v, int b, int l) {
+    if (p.desc.kind != QSV_STEP_PASS)
+        return false;
+    const int minR = b < v ? b : b + 1;
+    bool v_in_tile = false;
+    for (int q = 0; q < p.geom.L; ++q) {
+        if (q == v)
+            v_in_tile = true;
+        else if (q >= minR)
+            return false;
+    }
+    for (int i = 0; i < p.geom.nhigh; ++i) {
+        const int q = p.geom.high[i];
+        if (q == v)
+            v_in_tile = true;
+        else if (q >= minR)
+            return false;
+    }
+    if (v > minR && !v_in_tile)
+        return false;
+    return p.geom.K <= b + 1 && b + 1 < l;
+}
+
+int env_int(const char* name, int dflt) {
+    const char* s = std::getenv(name);
+    return s ? std::atoi(s) : dflt;
+}
+
+cudaError_t launch_step(qsv_state* st, qsv_program* prog, size_t i, uint64_t rank_base,
+                        const qsv::LaunchRange& rg = qsv::LaunchRange{}) {
+    const qsv::Step& s = prog->steps[i];
+    if (!prog->jit_of_step.empty() && prog->jit_of_step[i] >= 0)
+        return qsv::launch_jit(prog, st, i, prog->d_blobs + s.blob_off, rank_base, st->ctx->stream, rg);
+    return qsv::launch_pass(st, s, prog->d_blobs + s.blob_off, rank_base, st->ctx->stream, rg);
+}
+
 int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
     qsv_ctx* ctx = st->ctx;
     const uint64_t rank_base = static_cast<uint64_t>(ctx->rank) << st->n_local;
+    const bool overlap = evs == nullptr && env_int("QSV_OVERLAP", 1) != 0;
+    const int reserve = std::max(0, env_int("QSV_OVERLAP_RESERVE_SMS", 8));
     for (size_t i = 0; i < prog->steps.size(); ++i) {
         const qsv::Step& s = prog->steps[i];
         if (evs)
             QSV_CUDA(cudaEventRecord(evs[i], ctx->stream));
         if (s.desc.kind == QSV_STEP_PASS) {
-            if (!prog->jit_of_step.empty() && prog->jit_of_step[i] >= 0)
-                QSV_CUDA(qsv::launch_jit(prog, st, i, prog->d_blobs + s.blob_off, rank_base, ctx->stream));
-            else
-                QSV_CUDA(qsv::launch_pass(st, s, prog->d_blobs + s.blob_off, rank_base, ctx->stream));
-        } else {
+            QSV_CUDA(launch_step(st, prog, i, rank_base));
+            continue;
+        }
+        // swap: overlap the following region-compatible passes with its chunks
+        const int v = s.desc.swap_local, b = s.desc.chunk_log2, l = st->n_local;
+        size_t j = i + 1;
+        while (overlap && j < prog->steps.size() && region_pass_ok(prog->steps[j], v, b, l))
+            ++j;
+        if (j > i + 1) {
+            std::vector<cudaEvent_t> done;
+            const int rc = qsv::run_swap(st, s.desc.swap_global, v, b, s.desc.nbuf, &done);
+            if (rc != QSV_OK) {
+                for (cudaEvent_t e : done)
+                    cudaEventDestroy(e);
+                return rc;
+            }
+            const uint64_t C = done.size();
+            const int sms = std::max(1, ctx->sm_count - reserve);
+            cudaError_t err = cudaSuccess;
+            for (uint64_t c = 0; c < C && err == cudaSuccess; ++c) {
+                err = cudaStreamWaitEvent(ctx->stream, done[c], 0);
+                for (size_t p = i + 1; p < j && err == cudaSuccess; ++p) {
+                    const uint64_t T = st->size >> prog->steps[p].geom.K;
+                    qsv::LaunchRange rg;
+                    rg.tile0 = c * (T / C);
+                    rg.count = T / C;
+                    rg.sms = c + 1 < C ? sms : 0;  // the last region runs after the transfers
+                    err = launch_step(st, prog, p, rank_base, rg);
+                }
+            }
+            qsv::join_swap(ctx);
+            for (cudaEvent_t e : done)
+                cudaEventDestroy(e);
+            QSV_CUDA(err);
+            i = j - 1;
+            continue;
+        }
+        {
             const int rc = qsv::run_swap(st, s.desc.swap_global, s.desc.swap_local, s.desc.chunk_log2,
                                          s.desc.nbuf);
             if (rc != QSV_OK)

@@ -93,17 +93,28 @@ struct qsv_program {
 
 namespace qsv {
 void set_error(const std::string& msg);
+// Tile range and SM budget of one pass launch (default: every tile, every SM).
+struct LaunchRange {
+    uint64_t tile0 = 0;
+    uint64_t count = ~0ull;  // clipped to the pass's tile count
+    int sms = 0;             // 0: all SMs; else persistent grid over this many SMs
+};
 // Launches the pass kernel variant for `geom` on `st` (compute stream).
 cudaError_t launch_pass(const qsv_state* st, const Step& step, const unsigned char* d_blob,
-                        uint64_t rank_base, cudaStream_t stream);
+                        uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg = LaunchRange{});
 // NVRTC specialisation (jit.cu).
 bool jit_available(std::string& why);
 int jit_program(qsv_program* prog, int max_kernels, double* seconds);
 // Host-only: NVRTC-compiles the distinct pass kernels of compiled steps (no device).
 int jit_check(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels, int* kernels);
 cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step, const unsigned char* d_blob,
-                       uint64_t rank_base, cudaStream_t stream);
+                       uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg = LaunchRange{});
 void jit_release(qsv_program* prog);
 // Runs one chunked qubit swap (BBOP) of `st` with its peer; see qsv_swap.
-int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf);
+// With `chunk_done`, one event per chunk (recorded when the chunk's region is
+// final) is appended and the join with the compute stream is left to the caller
+// (join_swap), so that region passes can start chunk by chunk (BBOP overlap).
+int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf,
+             std::vector<cudaEvent_t>* chunk_done = nullptr);
+void join_swap(qsv_ctx* ctx);
 } // namespace qsv

@@ -56,7 +56,14 @@ int fail_nccl(const char* what, ncclResult_t r) {
 
 } // namespace
 
-int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf) {
+void join_swap(qsv_ctx* ctx) {
+    cudaEventRecord(ctx->ev_a, ctx->comm_stream);
+    cudaEventRecord(ctx->ev_b, ctx->copy_stream);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_a, 0);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
+}
+
+int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<cudaEvent_t>* chunk_done) {
     qsv_ctx* ctx = st->ctx;
     const int l = st->n_local;
     int m = 0;
@@ -143,12 +150,18 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf) {
                                                                   sendbit);
         }
         cudaEventRecord(free_ev[b], ctx->copy_stream);
+        if (chunk_done) {
+            // region c of the shard (half-index chunk c, both values of bit v) is final
+            cudaEvent_t ev;
+            cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            cudaEventRecord(ev, ctx->copy_stream);
+            chunk_done->push_back(ev);
+        }
     }
-    // join: the compute stream continues after both helper streams
-    cudaEventRecord(ctx->ev_a, ctx->comm_stream);
-    cudaEventRecord(ctx->ev_b, ctx->copy_stream);
-    cudaStreamWaitEvent(ctx->stream, ctx->ev_a, 0);
-    cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
+    // join: the compute stream continues after both helper streams (deferred to
+    // the caller when it overlaps region passes with the chunks)
+    if (!chunk_done)
+        join_swap(ctx);
     for (int b = 0; b < nbuf; ++b) {
         cudaEventDestroy(recv_ev[b]);
         cudaEventDestroy(free_ev[b]);
