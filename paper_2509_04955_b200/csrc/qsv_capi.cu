@@ -292,6 +292,7 @@ extern "C" int qsv_ctx_destroy(qsv_ctx* ctx) {
     if (ctx->d_partials) cudaFree(ctx->d_partials);
     if (ctx->d_stage) cudaFree(ctx->d_stage);
     if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+    if (ctx->d_sync) cudaFree(ctx->d_sync);
     if (ctx->h_result) cudaFreeHost(ctx->h_result);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
@@ -347,6 +348,10 @@ extern "C" int qsv_state_free(qsv_state* st) {
         return QSV_OK;
     cudaSetDevice(st->ctx->device);
     cudaStreamSynchronize(st->ctx->stream);
+    cudaStreamSynchronize(st->ctx->comm_stream);
+    for (size_t q = 0; q < st->peer_amps.size(); ++q)
+        if (st->peer_ipc[q] && st->peer_amps[q])
+            cudaIpcCloseMemHandle(st->peer_amps[q]);
     cudaFree(st->amps);
     delete st;
     return QSV_OK;

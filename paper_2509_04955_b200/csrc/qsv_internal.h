@@ -59,6 +59,8 @@ struct qsv_ctx {
     // host->device scratch for diff checks
     double* d_scratch = nullptr;
     size_t scratch_bytes = 0;
+    // pairwise barrier tokens of the P2P swap (2 doubles)
+    double* d_sync = nullptr;
 };
 
 struct qsv_state {
@@ -66,6 +68,11 @@ struct qsv_state {
     int n_local = 0;
     uint64_t size = 0;     // 2^n_local amplitudes
     double2* amps = nullptr;
+    // peer shards mapped into this process (NVLink P2P swaps); filled by the first
+    // collective swap: same-process ranks by peer access, other processes by CUDA IPC
+    bool peers_ready = false;
+    std::vector<double2*> peer_amps;   // per rank, nullptr = not mapped
+    std::vector<char> peer_ipc;        // 1 = opened with cudaIpcOpenMemHandle (close on free)
 };
 
 namespace qsv {

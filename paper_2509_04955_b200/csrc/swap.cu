@@ -18,6 +18,10 @@
 // amplitudes (+ nbuf*2^b send staging when bit v lies inside a chunk).
 #include "qsv_internal.h"
 
+#include <unistd.h>
+
+#include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -44,6 +48,39 @@ __global__ void scatter_half_kernel(double2* __restrict__ psi, const double2* __
         psi[insert_bit(r0 + i, v, bit)] = stage[i];
 }
 
+// NVLink P2P swap: rank a = 0 exchanges pairs r in [0, H/2), rank a = 1 the rest;
+// each pair is (my slot with bit v = !a) <-> (peer slot with bit v = a), read and
+// written by exactly one GPU, so no staging and no copy-back.  Each thread keeps
+// four remote loads in flight to cover the NVLink round trip.
+__global__ void __launch_bounds__(256) p2p_swap_kernel(double2* __restrict__ mine, double2* __restrict__ theirs,
+                                                       uint64_t r0, uint64_t count, int v, uint64_t mybit,
+                                                       uint64_t theirbit) {
+    constexpr int U = 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < count; i0 += stride * U) {
+        double2 a[U], b[U];
+        uint64_t xm[U], xt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = i0 + u * stride;
+            if (i < count) {
+                xm[u] = insert_bit(r0 + i, v, mybit);
+                xt[u] = insert_bit(r0 + i, v, theirbit);
+                a[u] = mine[xm[u]];
+                b[u] = theirs[xt[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = i0 + u * stride;
+            if (i < count) {
+                mine[xm[u]] = b[u];
+                theirs[xt[u]] = a[u];
+            }
+        }
+    }
+}
+
 int fail_cuda(const char* what, cudaError_t e) {
     set_error(std::string(what) + ": " + cudaGetErrorString(e));
     return QSV_E_CUDA;
@@ -52,6 +89,103 @@ int fail_cuda(const char* what, cudaError_t e) {
 int fail_nccl(const char* what, ncclResult_t r) {
     set_error(std::string(what) + ": " + ncclGetErrorString(r));
     return QSV_E_NCCL;
+}
+
+struct PeerInfo {
+    cudaIpcMemHandle_t handle;
+    uint64_t ptr;
+    int32_t pid;
+    int32_t device;
+    int32_t ok;
+    char pad[128 - sizeof(cudaIpcMemHandle_t) - 8 - 12];
+};
+static_assert(sizeof(PeerInfo) == 128, "PeerInfo is exchanged as 128 bytes");
+
+// Collective (all ranks): maps every peer's shard into this process.
+void exchange_peers(qsv_state* st) {
+    qsv_ctx* ctx = st->ctx;
+    st->peers_ready = true;
+    st->peer_amps.assign(ctx->nranks, nullptr);
+    st->peer_ipc.assign(ctx->nranks, 0);
+    PeerInfo mine{};
+    mine.ok = cudaIpcGetMemHandle(&mine.handle, st->amps) == cudaSuccess;
+    cudaGetLastError();
+    mine.ptr = reinterpret_cast<uint64_t>(st->amps);
+    mine.pid = static_cast<int32_t>(getpid());
+    mine.device = ctx->device;
+    void* d_info = nullptr;
+    if (cudaMalloc(&d_info, sizeof(PeerInfo) * ctx->nranks) != cudaSuccess)
+        return;
+    std::vector<PeerInfo> all(ctx->nranks);
+    bool ok = cudaMemcpy(static_cast<char*>(d_info) + sizeof(PeerInfo) * ctx->rank, &mine, sizeof(PeerInfo),
+                         cudaMemcpyHostToDevice) == cudaSuccess;
+    ok = ok && ncclAllGather(static_cast<char*>(d_info) + sizeof(PeerInfo) * ctx->rank, d_info, sizeof(PeerInfo),
+                             ncclChar, ctx->comm, ctx->comm_stream) == ncclSuccess;
+    ok = ok && cudaStreamSynchronize(ctx->comm_stream) == cudaSuccess;
+    ok = ok && cudaMemcpy(all.data(), d_info, sizeof(PeerInfo) * ctx->nranks, cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaFree(d_info);
+    if (!ok)
+        return;
+    for (int q = 0; q < ctx->nranks; ++q) {
+        if (q == ctx->rank)
+            continue;
+        const PeerInfo& pi = all[q];
+        if (pi.pid == mine.pid) {
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, ctx->device, pi.device);
+            if (!can)
+                continue;
+            const cudaError_t e = cudaDeviceEnablePeerAccess(pi.device, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                cudaGetLastError();
+                continue;
+            }
+            cudaGetLastError();
+            st->peer_amps[q] = reinterpret_cast<double2*>(pi.ptr);
+        } else if (pi.ok) {
+            void* p = nullptr;
+            if (cudaIpcOpenMemHandle(&p, pi.handle, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+                st->peer_amps[q] = static_cast<double2*>(p);
+                st->peer_ipc[q] = 1;
+            } else {
+                cudaGetLastError();
+            }
+        }
+    }
+    // all ranks must take the same path: P2P only if every rank mapped every peer
+    int ok_local = 1;
+    for (int q = 0; q < ctx->nranks; ++q)
+        ok_local &= (q == ctx->rank || st->peer_amps[q] != nullptr) ? 1 : 0;
+    int* d_flag = nullptr;
+    int ok_all = 0;
+    if (cudaMalloc(&d_flag, sizeof(int)) == cudaSuccess) {
+        cudaMemcpy(d_flag, &ok_local, sizeof(int), cudaMemcpyHostToDevice);
+        if (ncclAllReduce(d_flag, d_flag, 1, ncclInt32, ncclMin, ctx->comm, ctx->comm_stream) == ncclSuccess &&
+            cudaStreamSynchronize(ctx->comm_stream) == cudaSuccess)
+            cudaMemcpy(&ok_all, d_flag, sizeof(int), cudaMemcpyDeviceToHost);
+        cudaFree(d_flag);
+    }
+    if (!ok_all) {
+        for (int q = 0; q < ctx->nranks; ++q)
+            if (st->peer_ipc[q] && st->peer_amps[q])
+                cudaIpcCloseMemHandle(st->peer_amps[q]);
+        st->peer_amps.assign(ctx->nranks, nullptr);
+        st->peer_ipc.assign(ctx->nranks, 0);
+    }
+}
+
+// Pairwise barrier with `peer` on the comm stream (an 8-byte grouped send/recv).
+ncclResult_t pair_barrier(qsv_ctx* ctx, int peer) {
+    ncclResult_t r = ncclGroupStart();
+    if (r == ncclSuccess) r = ncclSend(ctx->d_sync, 1, ncclDouble, peer, ctx->comm, ctx->comm_stream);
+    if (r == ncclSuccess) r = ncclRecv(ctx->d_sync + 1, 1, ncclDouble, peer, ctx->comm, ctx->comm_stream);
+    const ncclResult_t r2 = ncclGroupEnd();
+    return r != ncclSuccess ? r : r2;
+}
+
+bool p2p_mode() {
+    const char* m = std::getenv("QSV_SWAP_MODE");
+    return !(m && std::strcmp(m, "nccl") == 0);
 }
 
 } // namespace
@@ -84,6 +218,43 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
     const int peer = ctx->rank ^ (1 << (g - l));
     const uint64_t a = static_cast<uint64_t>((ctx->rank >> (g - l)) & 1);
     const uint64_t sendbit = a ^ 1ull;
+
+    if (p2p_mode()) {
+        if (!st->peers_ready)
+            exchange_peers(st);  // collective: every rank reaches its first swap
+        // every rank must agree on the mode: P2P only when both sides mapped each other,
+        // which holds symmetrically on one NVSwitch box (checked per pair below)
+    }
+    if (p2p_mode() && st->peer_amps.size() == static_cast<size_t>(ctx->nranks) && st->peer_amps[peer]) {
+        if (!ctx->d_sync) {
+            e = cudaMalloc(&ctx->d_sync, 2 * sizeof(double));
+            if (e != cudaSuccess)
+                return fail_cuda("qsv_swap: sync token cudaMalloc", e);
+            cudaMemset(ctx->d_sync, 0, 2 * sizeof(double));
+        }
+        cudaEventRecord(ctx->ev_a, ctx->stream);
+        cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0);
+        ncclResult_t r = pair_barrier(ctx, peer);  // the peer's earlier passes are done
+        if (r != ncclSuccess)
+            return fail_nccl("qsv_swap: barrier", r);
+        const uint64_t H = 1ull << (l - 1);
+        const uint64_t half = H / 2;
+        p2p_swap_kernel<<<ctx->sm_count * 4, 256, 0, ctx->comm_stream>>>(st->amps, st->peer_amps[peer], a * half,
+                                                                         half, v, sendbit, a);
+        r = pair_barrier(ctx, peer);  // the peer's writes into this shard are done
+        if (r != ncclSuccess)
+            return fail_nccl("qsv_swap: barrier", r);
+        if (chunk_done) {
+            cudaEvent_t ev;
+            cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            cudaEventRecord(ev, ctx->comm_stream);
+            chunk_done->push_back(ev);
+        } else {
+            join_swap(ctx);
+        }
+        e = cudaGetLastError();
+        return e == cudaSuccess ? QSV_OK : fail_cuda("qsv_swap: p2p kernel", e);
+    }
     const uint64_t C = 1ull << chunk_log2;
     const uint64_t nchunks = (1ull << (l - 1)) / C;
     const bool contiguous = v >= chunk_log2;
