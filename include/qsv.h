@@ -46,6 +46,7 @@ extern "C" {
 #define QSV_MAX_DENSE_K 5   /* largest dense fused block (32x32 complex)     */
 #define QSV_MAX_DIAG_K 8    /* largest tabulated diagonal block              */
 #define QSV_MAX_HIGH 8      /* high (non-contiguous) tile qubits per pass    */
+#define QSV_MAX_TILE_K 12   /* tile qubits per pass (12 only with specialised kernels) */
 #define QSV_NCCL_ID_BYTES 128
 
 typedef struct qsv_ctx qsv_ctx;         /* one GPU + its stream(s) + comm   */

@@ -1260,8 +1260,8 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     c.validate();
     if (opt.fuse_k < 1 || opt.fuse_k > QSV_MAX_DENSE_K)
         throw std::invalid_argument("make_plan: fuse_k must be in [1, 5]");
-    if (opt.tile_k < 1 || opt.tile_k > 11)
-        throw std::invalid_argument("make_plan: tile_k must be in [1, 11]");
+    if (opt.tile_k < 1 || opt.tile_k > QSV_MAX_TILE_K)
+        throw std::invalid_argument("make_plan: tile_k must be in [1, 12] (12 needs the specialised kernels)");
     if (opt.rblock_k != 3 && opt.rblock_k != 4)
         throw std::invalid_argument("make_plan: rblock_k must be 3 or 4");
     Plan plan;

@@ -20,6 +20,7 @@ typedef unsigned long long uint64_t;
 #define QSV_MAX_DENSE_K 5
 #define QSV_MAX_DIAG_K 8
 #define QSV_MAX_HIGH 8
+#define QSV_MAX_TILE_K 12
 #define QSV_OP_DENSE 0
 #define QSV_OP_DIAG 1
 #define QSV_OP_XPERM 2

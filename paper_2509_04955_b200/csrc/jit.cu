@@ -115,7 +115,7 @@ const Driver& driver() {
 }
 
 // ------------------------------------------------------------------ codegen
-int threads_for_k(int K) { return K >= 8 ? 128 : (K >= 6 ? 64 : 32); }
+int threads_for_k(int K) { return K >= 12 ? 256 : (K >= 8 ? 128 : (K >= 6 ? 64 : 32)); }
 
 std::string u32(uint32_t x) {
     std::ostringstream o;
@@ -135,7 +135,7 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
     const int NT = threads_for_k(K);
     const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
     std::ostringstream o;
-    minb = 3;
+    minb = K >= 12 ? 1 : 3;
     for (int i = 0; i < s.nops; ++i) {
         const TileOp& op = ops[i];
         const std::string opref = "*reinterpret_cast<const qsv::TileOp*>(blob + " +

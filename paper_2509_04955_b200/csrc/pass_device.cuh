@@ -177,7 +177,7 @@ template <int K, int NT>
 __device__ __forceinline__ void relabel_op(double2* __restrict__ tile, const TileOp& op,
                                            const unsigned char* blob) {
     constexpr int TILE = 1 << K;
-    constexpr int TB = NT >= 128 ? 7 : (NT >= 64 ? 6 : 5);
+    constexpr int TB = NT >= 256 ? 8 : (NT >= 128 ? 7 : (NT >= 64 ? 6 : 5));
     const uint16_t* col = reinterpret_cast<const uint16_t*>(blob + op.mat_byte);
     if constexpr (TILE >= NT) {
         constexpr int APT = TILE / NT;

@@ -498,7 +498,9 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                  std::vector<unsigned char>& blob_out) {
     using qsv::TileOp;
     const int K = d.tile_k;
-    QSV_REQUIRE(K >= 1 && K <= 11 && K <= n_local, "pass: tile_k must be in [1, min(11, n_local)]");
+    QSV_REQUIRE(K >= 1 && K <= QSV_MAX_TILE_K && K <= n_local,
+                "pass: tile_k must be in [1, min(12, n_local)] (12: specialised kernels only)");
+    const int nhi = K > 5 ? 1 << (K - 5) : 1;  // entries of the high-tile-bit tables
     QSV_REQUIRE(d.nhigh >= 0 && d.nhigh <= QSV_MAX_HIGH && d.nhigh <= K, "pass: bad nhigh");
     const int L = K - d.nhigh;
     int tpos_of[64];
@@ -685,9 +687,9 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                         "op: PHASEPROD primitive range outside the primitive array");
             QSV_REQUIRE(od.mat_off >= 0 && static_cast<size_t>(od.mat_off) + 1 <= pool_len,
                         "op: PHASEPROD constant outside the pool");
-            // table: [c][A: 32 low tile bits][B: 64 high tile bits]
-            std::vector<double> tab(2 * 97, 0.0);
-            for (int e = 0; e < 97; ++e)
+            // table: [c][A: 32 low tile bits][B: 2^(K-5) high tile bits]
+            std::vector<double> tab(2 * (33 + nhi), 0.0);
+            for (int e = 0; e < 33 + nhi; ++e)
                 tab[2 * e] = 1.0;
             tab[0] = pool[2 * od.mat_off];
             tab[1] = pool[2 * od.mat_off + 1];
@@ -710,7 +712,7 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                         if (e >> tp & 1)
                             mul_into(1 + e, fr, fi);
                 } else if (tp >= 5) {
-                    for (int e = 0; e < 64; ++e)
+                    for (int e = 0; e < nhi; ++e)
                         if (e >> (tp - 5) & 1)
                             mul_into(33 + e, fr, fi);
                 } else {
@@ -810,9 +812,9 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
             t.fmask |= 1u << fix[i];
         }
         if (od.kind == QSV_OP_DIAG && t.nin > 0) {
-            // pext(idx, tmask) = ptab_lo[idx & 31] | ptab_hi[idx >> 5]  (K <= 11)
-            pl.ptab.resize(96);
-            for (int j = 0; j < 96; ++j) {
+            // pext(idx, tmask) = ptab_lo[idx & 31] | ptab_hi[idx >> 5]
+            pl.ptab.resize(32 + nhi);
+            for (int j = 0; j < 32 + nhi; ++j) {
                 const uint32_t idx = j < 32 ? static_cast<uint32_t>(j) : static_cast<uint32_t>(j - 32) << 5;
                 uint32_t e = 0, m = t.tmask;
                 for (int bit = 0; m; ++bit) {

@@ -44,6 +44,7 @@ OPTS = {
     "relabel": pkg.PlanOptions(relabel=2),
     "relabel-t8": pkg.PlanOptions(relabel=2, tile_k=8, min_low=4),
     "relabel-interp": pkg.PlanOptions(relabel=2, tile_k=7, min_low=3, jit=False),
+    "tile12": pkg.PlanOptions(tile_k=12, pass_budget=100),
 }
 
 

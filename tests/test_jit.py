@@ -26,6 +26,8 @@ CASES = [
     ("hea:15:3:4", dict(rblock_k=3)),
     ("random:14:6:2", dict(register_blocks=False, fuse_k=4, tile_k=10)),
     ("random:14:6:2", dict(register_blocks=False, fuse_k=5, pass_budget=500)),
+    ("random:16:8:2", dict(tile_k=12, relabel=2)),
+    ("qft:16", dict(tile_k=12)),
 ]
 
 
