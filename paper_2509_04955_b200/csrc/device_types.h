@@ -91,6 +91,11 @@ struct GeomArg {
     int32_t L, nhigh;
     int32_t high[QSV_MAX_HIGH];
     uint64_t tile0;  // first tile of the launch (region launches overlapped with a swap)
+    // region launch: tiles whose bits reg[0..nreg) (ascending, outside the tile) equal
+    // rval; the tile index then enumerates the remaining bits only
+    int32_t nreg;
+    int32_t reg[3];
+    uint64_t rval;
 };
 
 // Largest per-pass blob (bytes of shared memory on top of the tile buffers).

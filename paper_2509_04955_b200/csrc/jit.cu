@@ -584,8 +584,9 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
     for (int i = 0; i < s.geom.nhigh; ++i)
         ga.high[i] = s.geom.high[i];
     const uint64_t all_tiles = st->size >> s.geom.K;
-    ga.tile0 = std::min(rg.tile0, all_tiles);
-    const uint64_t tiles = std::min(rg.count, all_tiles - ga.tile0);
+    const uint64_t region_tiles = apply_region(ga, rg, all_tiles);
+    ga.tile0 = std::min(rg.tile0, region_tiles);
+    const uint64_t tiles = std::min(rg.count, region_tiles - ga.tile0);
     if (tiles == 0)
         return cudaSuccess;
     const int sms = rg.sms > 0 ? std::min(rg.sms, st->ctx->sm_count) : st->ctx->sm_count;

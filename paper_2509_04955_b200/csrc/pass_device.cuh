@@ -641,12 +641,18 @@ __device__ __forceinline__ void phaseprod_op(double2* tile, const TileOp& op, co
 
 __device__ __forceinline__ uint64_t tile_base(uint64_t t, const GeomArg& g) {
     uint64_t base = t << g.L;
-    for (int i = 0; i < g.nhigh; ++i) {
-        const int h = g.high[i];
+    // insert zeros at the high tile bits and the region bits, ascending
+    int i = 0, j = 0;
+    while (i < g.nhigh || j < g.nreg) {
+        int h;
+        if (j >= g.nreg || (i < g.nhigh && g.high[i] < g.reg[j]))
+            h = g.high[i++];
+        else
+            h = g.reg[j++];
         const uint64_t lo = base & ((1ull << h) - 1ull);
         base = ((base ^ lo) << 1) | lo;
     }
-    return base;
+    return base | g.rval;
 }
 
 // The persistent TMA pipeline of a pass; `ops(tile, blob, full_base)` applies

@@ -122,8 +122,9 @@ cudaError_t launch_variant(const qsv_state* st, const Step& step, const unsigned
     for (int i = 0; i < step.geom.nhigh; ++i)
         ga.high[i] = step.geom.high[i];
     const uint64_t all_tiles = st->size >> K;
-    ga.tile0 = std::min(rg.tile0, all_tiles);
-    const uint64_t tiles = std::min(rg.count, all_tiles - ga.tile0);
+    const uint64_t region_tiles = apply_region(ga, rg, all_tiles);
+    ga.tile0 = std::min(rg.tile0, region_tiles);
+    const uint64_t tiles = std::min(rg.count, region_tiles - ga.tile0);
     if (tiles == 0)
         return cudaSuccess;
     const int sms = rg.sms > 0 ? std::min(rg.sms, sm_count) : sm_count;
@@ -151,6 +152,15 @@ cudaError_t launch_k(const qsv_state* st, const Step& step, const unsigned char*
 }
 
 } // namespace
+
+uint64_t apply_region(GeomArg& ga, const LaunchRange& rg, uint64_t all_tiles) {
+    ga.nreg = 0;
+    ga.rval = rg.rval & rg.rmask;
+    for (int b = 0; b < 64 && ga.nreg < 3; ++b)
+        if ((rg.rmask >> b) & 1ull)
+            ga.reg[ga.nreg++] = b;
+    return all_tiles >> ga.nreg;
+}
 
 cudaError_t launch_pass(const qsv_state* st, const Step& step, const unsigned char* d_blob,
                         uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg) {

@@ -1123,6 +1123,71 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
         }
         // swap: overlap the following region-compatible passes with its chunks
         const int v = s.desc.swap_local, b = s.desc.chunk_log2, l = st->n_local;
+        if (overlap && qsv::p2p_swap_ready(st, s.desc.swap_global)) {
+            // NVLink P2P: any two local bits outside the next passes' tiles can split
+            // the swap into 4 regions; pick the pair that covers the most passes
+            auto tile_mask = [&](const qsv::Step& p) {
+                uint64_t m = (1ull << p.geom.L) - 1ull;
+                for (int h = 0; h < p.geom.nhigh; ++h)
+                    m |= 1ull << p.geom.high[h];
+                return m;
+            };
+            int best_k = 0;
+            uint64_t best_mask = 0;
+            for (int b1 = l - 1; b1 >= 5; --b1)
+                for (int b2 = b1 - 1; b2 >= 5; --b2) {
+                    if (b1 == v || b2 == v)
+                        continue;
+                    const uint64_t rm = (1ull << b1) | (1ull << b2);
+                    int k = 0;
+                    for (size_t q = i + 1; q < prog->steps.size(); ++q) {
+                        const qsv::Step& p = prog->steps[q];
+                        if (p.desc.kind != QSV_STEP_PASS || (tile_mask(p) & rm) || p.geom.K + 2 > l - 1)
+                            break;
+                        ++k;
+                    }
+                    if (k > best_k) {
+                        best_k = k;
+                        best_mask = rm;
+                    }
+                }
+            if (best_k > 0) {
+                std::vector<cudaEvent_t> done;
+                const int rc = qsv::run_swap(st, s.desc.swap_global, v, b, s.desc.nbuf, &done, best_mask);
+                if (rc != QSV_OK) {
+                    for (cudaEvent_t e : done)
+                        cudaEventDestroy(e);
+                    return rc;
+                }
+                const int swap_sms = std::max(1, std::min(ctx->sm_count - 1, env_int("QSV_SWAP_SMS", 32)));
+                cudaError_t err = cudaSuccess;
+                int rb[2], nr = 0;
+                for (int q = 0; q < l && nr < 2; ++q)
+                    if ((best_mask >> q) & 1ull)
+                        rb[nr++] = q;
+                for (uint64_t c = 0; c < done.size() && err == cudaSuccess; ++c) {
+                    err = cudaStreamWaitEvent(ctx->stream, done[c], 0);
+                    qsv::LaunchRange rg;
+                    rg.rmask = best_mask;
+                    rg.rval = 0;
+                    for (int q = 0; q < nr; ++q)
+                        rg.rval |= ((c >> q) & 1ull) << rb[q];
+                    rg.sms = c + 1 < done.size() ? ctx->sm_count - swap_sms : 0;
+                    for (size_t p = i + 1; p <= i + static_cast<size_t>(best_k) && err == cudaSuccess; ++p)
+                        err = launch_step(st, prog, p, rank_base, rg);
+                }
+                qsv::join_swap(ctx);
+                for (cudaEvent_t e : done)
+                    cudaEventDestroy(e);
+                QSV_CUDA(err);
+                i += static_cast<size_t>(best_k);
+                continue;
+            }
+            const int rc = qsv::run_swap(st, s.desc.swap_global, v, b, s.desc.nbuf);
+            if (rc != QSV_OK)
+                return rc;
+            continue;
+        }
         size_t j = i + 1;
         while (overlap && j < prog->steps.size() && region_pass_ok(prog->steps[j], v, b, l))
             ++j;

@@ -105,7 +105,11 @@ struct LaunchRange {
     uint64_t tile0 = 0;
     uint64_t count = ~0ull;  // clipped to the pass's tile count
     int sms = 0;             // 0: all SMs; else persistent grid over this many SMs
+    uint64_t rmask = 0;      // region bits (<= 3, outside the pass's tile)
+    uint64_t rval = 0;       // their values (a subset of rmask)
 };
+// Fills the region fields of `ga` from rg; returns the number of tiles of the region.
+uint64_t apply_region(GeomArg& ga, const LaunchRange& rg, uint64_t all_tiles);
 // Launches the pass kernel variant for `geom` on `st` (compute stream).
 cudaError_t launch_pass(const qsv_state* st, const Step& step, const unsigned char* d_blob,
                         uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg = LaunchRange{});
@@ -121,7 +125,11 @@ void jit_release(qsv_program* prog);
 // With `chunk_done`, one event per chunk (recorded when the chunk's region is
 // final) is appended and the join with the compute stream is left to the caller
 // (join_swap), so that region passes can start chunk by chunk (BBOP overlap).
+// P2P mode: `region_mask` (<= 2 local bits, not v) splits the swap into regions, one
+// event each; otherwise chunks follow the NCCL top-bit order.
 int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf,
-             std::vector<cudaEvent_t>* chunk_done = nullptr);
+             std::vector<cudaEvent_t>* chunk_done = nullptr, uint64_t region_mask = 0);
+// Collective on first use: maps the peers' shards; true when swap g will use NVLink P2P.
+bool p2p_swap_ready(qsv_state* st, int g);
 void join_swap(qsv_ctx* ctx);
 } // namespace qsv

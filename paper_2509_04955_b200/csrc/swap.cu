@@ -81,6 +81,50 @@ __global__ void __launch_bounds__(256) p2p_swap_kernel(double2* __restrict__ min
     }
 }
 
+__device__ __forceinline__ uint64_t insert_zero(uint64_t x, int p) {
+    const uint64_t lo = x & ((1ull << p) - 1ull);
+    return ((x ^ lo) << 1) | lo;
+}
+
+// Region form of the P2P swap: pairs whose region bits equal `rval`.  Bit positions
+// pos[0..npos) (ascending: v and the region bits) are inserted as zeros into the
+// pair index, then the region value and the two values of bit v are ORed in.
+__global__ void __launch_bounds__(256) p2p_swap_region_kernel(double2* __restrict__ mine,
+                                                              double2* __restrict__ theirs, uint64_t i_begin,
+                                                              uint64_t count, int p0, int p1, int p2, int npos,
+                                                              uint64_t rval, uint64_t mine_v, uint64_t theirs_v) {
+    constexpr int U = 4;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < count; i0 += stride * U) {
+        double2 a[U], b[U];
+        uint64_t xm[U], xt[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = i0 + u * stride;
+            if (i < count) {
+                uint64_t x = insert_zero(i_begin + i, p0);
+                if (npos > 1)
+                    x = insert_zero(x, p1);
+                if (npos > 2)
+                    x = insert_zero(x, p2);
+                x |= rval;
+                xm[u] = x | mine_v;
+                xt[u] = x | theirs_v;
+                a[u] = mine[xm[u]];
+                b[u] = theirs[xt[u]];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint64_t i = i0 + u * stride;
+            if (i < count) {
+                mine[xm[u]] = b[u];
+                theirs[xt[u]] = a[u];
+            }
+        }
+    }
+}
+
 int fail_cuda(const char* what, cudaError_t e) {
     set_error(std::string(what) + ": " + cudaGetErrorString(e));
     return QSV_E_CUDA;
@@ -183,6 +227,11 @@ ncclResult_t pair_barrier(qsv_ctx* ctx, int peer) {
     return r != ncclSuccess ? r : r2;
 }
 
+int env_int_swap(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+
 bool p2p_mode() {
     const char* m = std::getenv("QSV_SWAP_MODE");
     return !(m && std::strcmp(m, "nccl") == 0);
@@ -197,7 +246,19 @@ void join_swap(qsv_ctx* ctx) {
     cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
 }
 
-int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<cudaEvent_t>* chunk_done) {
+bool p2p_swap_ready(qsv_state* st, int g) {
+    qsv_ctx* ctx = st->ctx;
+    if (!p2p_mode() || ctx->nranks < 2 || ctx->comm == nullptr)
+        return false;
+    if (!st->peers_ready)
+        exchange_peers(st);  // collective: every rank reaches the same swap
+    const int l = st->n_local;
+    const int peer = ctx->rank ^ (1 << (g - l));
+    return st->peer_amps.size() == static_cast<size_t>(ctx->nranks) && peer < ctx->nranks && st->peer_amps[peer];
+}
+
+int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<cudaEvent_t>* chunk_done,
+             uint64_t region_mask) {
     qsv_ctx* ctx = st->ctx;
     const int l = st->n_local;
     int m = 0;
@@ -239,18 +300,48 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
             return fail_nccl("qsv_swap: barrier", r);
         const uint64_t H = 1ull << (l - 1);
         const uint64_t half = H / 2;
-        p2p_swap_kernel<<<ctx->sm_count * 4, 256, 0, ctx->comm_stream>>>(st->amps, st->peer_amps[peer], a * half,
-                                                                         half, v, sendbit, a);
-        r = pair_barrier(ctx, peer);  // the peer's writes into this shard are done
-        if (r != ncclSuccess)
-            return fail_nccl("qsv_swap: barrier", r);
-        if (chunk_done) {
-            cudaEvent_t ev;
-            cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-            cudaEventRecord(ev, ctx->comm_stream);
-            chunk_done->push_back(ev);
+        region_mask &= ~(1ull << v);
+        if (!chunk_done || region_mask == 0) {
+            p2p_swap_kernel<<<ctx->sm_count * 4, 256, 0, ctx->comm_stream>>>(st->amps, st->peer_amps[peer],
+                                                                             a * half, half, v, sendbit, a);
+            r = pair_barrier(ctx, peer);  // the peer's writes into this shard are done
+            if (r != ncclSuccess)
+                return fail_nccl("qsv_swap: barrier", r);
+            if (chunk_done) {
+                cudaEvent_t ev;
+                cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+                cudaEventRecord(ev, ctx->comm_stream);
+                chunk_done->push_back(ev);
+            } else {
+                join_swap(ctx);
+            }
         } else {
-            join_swap(ctx);
+            // one kernel + pair barrier per region: region c is final when its event fires
+            int pos[3], npos = 0, rb[2], nr = 0;
+            for (int b = 0; b < l && npos < 3; ++b)
+                if (b == v || ((region_mask >> b) & 1ull)) {
+                    pos[npos++] = b;
+                    if (b != v)
+                        rb[nr++] = b;
+                }
+            const uint64_t pairs = H >> nr;  // per region, both ranks together
+            const uint64_t mine_half = pairs / 2;
+            const int sms = std::max(1, std::min(ctx->sm_count, env_int_swap("QSV_SWAP_SMS", 32)));
+            for (uint64_t c = 0; c < (1ull << nr); ++c) {
+                uint64_t rval = 0;
+                for (int i = 0; i < nr; ++i)
+                    rval |= ((c >> i) & 1ull) << rb[i];
+                p2p_swap_region_kernel<<<sms * 4, 256, 0, ctx->comm_stream>>>(
+                    st->amps, st->peer_amps[peer], a * mine_half, mine_half, pos[0], npos > 1 ? pos[1] : 0,
+                    npos > 2 ? pos[2] : 0, npos, rval, sendbit << v, a << v);
+                r = pair_barrier(ctx, peer);
+                if (r != ncclSuccess)
+                    return fail_nccl("qsv_swap: barrier", r);
+                cudaEvent_t ev;
+                cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+                cudaEventRecord(ev, ctx->comm_stream);
+                chunk_done->push_back(ev);
+            }
         }
         e = cudaGetLastError();
         return e == cudaSuccess ? QSV_OK : fail_cuda("qsv_swap: p2p kernel", e);
