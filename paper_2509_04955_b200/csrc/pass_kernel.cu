@@ -29,6 +29,7 @@
 // never force a qubit into the tile), XPERM (X / CX / Toffoli as an SMEM swap).
 // Tile-bit controls restrict the group enumeration (Alg. 4's half-work,
 // PAPER:238-257); out-of-tile controls are a CTA-uniform test of the tile base.
+#include <string>
 #include "qsv_internal.h"
 #include "pass_device.cuh"
 
@@ -176,7 +177,11 @@ cudaError_t launch_pass(const qsv_state* st, const Step& step, const unsigned ch
     case 9: return launch_k<9>(st, step, d_blob, rank_base, stream, rg);
     case 10: return launch_k<10>(st, step, d_blob, rank_base, stream, rg);
     case 11: return launch_k<11>(st, step, d_blob, rank_base, stream, rg);
-    default: return cudaErrorInvalidValue;
+    default:
+        set_error("pass: tile_k " + std::to_string(step.geom.K) +
+                  " has no interpreter kernel (only NVRTC-specialised kernels run tiles of 12 qubits; "
+                  "raise jit_max_kernels or use tile_k <= 11)");
+        return cudaErrorInvalidValue;
     }
 }
 

@@ -1108,79 +1108,169 @@ cudaError_t launch_step(qsv_state* st, qsv_program* prog, size_t i, uint64_t ran
     return qsv::launch_pass(st, s, prog->d_blobs + s.blob_off, rank_base, st->ctx->stream, rg);
 }
 
+uint64_t tile_mask(const qsv::Step& p) {
+    uint64_t m = (1ull << p.geom.L) - 1ull;
+    for (int h = 0; h < p.geom.nhigh; ++h)
+        m |= 1ull << p.geom.high[h];
+    return m;
+}
+
+// BBOP over NVLink P2P: a swap split into 4 regions (two local bits outside the tiles
+// of the passes around it) overlaps the passes before it (region c of the swap starts
+// once region c of those passes is written) and after it (region c of those passes
+// starts once region c of the swap has landed).
+struct SwapOverlap {
+    uint64_t rmask = 0;
+    size_t pre_begin = 0;  // passes [pre_begin, swap) run region by region before it
+    size_t post_end = 0;   // passes (swap, post_end] run region by region after it
+};
+
+std::map<size_t, SwapOverlap> plan_overlap(const qsv_program* prog, int l) {
+    std::map<size_t, SwapOverlap> plans;
+    size_t free_from = 0;  // first step not claimed by an earlier swap's post range
+    const size_t n = prog->steps.size();
+    for (size_t i = 0; i < n; ++i) {
+        const qsv::Step& s = prog->steps[i];
+        if (s.desc.kind != QSV_STEP_SWAP)
+            continue;
+        const int v = s.desc.swap_local;
+        int best = 0;
+        SwapOverlap bp;
+        for (int b1 = l - 1; b1 >= 5; --b1)
+            for (int b2 = b1 - 1; b2 >= 5; --b2) {
+                if (b1 == v || b2 == v)
+                    continue;
+                const uint64_t rm = (1ull << b1) | (1ull << b2);
+                auto ok = [&](const qsv::Step& p) {
+                    return p.desc.kind == QSV_STEP_PASS && !(tile_mask(p) & rm) && p.geom.K + 2 <= l - 1;
+                };
+                size_t pre = i;
+                while (pre > free_from && ok(prog->steps[pre - 1]))
+                    --pre;
+                size_t post = i;
+                while (post + 1 < n && ok(prog->steps[post + 1]))
+                    ++post;
+                const int k = static_cast<int>((i - pre) + (post - i));
+                if (k > best) {
+                    best = k;
+                    bp.rmask = rm;
+                    bp.pre_begin = pre;
+                    bp.post_end = post;
+                }
+            }
+        if (best > 0) {
+            plans[i] = bp;
+            free_from = bp.post_end + 1;
+        } else {
+            free_from = i + 1;
+        }
+    }
+    return plans;
+}
+
 int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
     qsv_ctx* ctx = st->ctx;
     const uint64_t rank_base = static_cast<uint64_t>(ctx->rank) << st->n_local;
     const bool overlap = evs == nullptr && env_int("QSV_OVERLAP", 1) != 0;
     const int reserve = std::max(0, env_int("QSV_OVERLAP_RESERVE_SMS", 8));
+    const int l = st->n_local;
+    // P2P region schedule (collective check on the first swap: all ranks agree)
+    std::map<size_t, SwapOverlap> p2p_plan;
+    bool p2p = false;
+    if (overlap && prog->has_collective) {
+        for (const qsv::Step& s : prog->steps)
+            if (s.desc.kind == QSV_STEP_SWAP) {
+                p2p = qsv::p2p_swap_ready(st, s.desc.swap_global);
+                break;
+            }
+        if (p2p)
+            p2p_plan = plan_overlap(prog, l);
+    }
+    const int swap_sms = std::max(1, std::min(ctx->sm_count - 1, env_int("QSV_SWAP_SMS", 16)));
+    auto region_of = [&](uint64_t rm, uint64_t c) {
+        qsv::LaunchRange rg;
+        rg.rmask = rm;
+        int k = 0;
+        for (int q = 0; q < 64; ++q)
+            if ((rm >> q) & 1ull)
+                rg.rval |= ((c >> k++) & 1ull) << q;
+        return rg;
+    };
+    // pre-pass start index -> swap index
+    std::map<size_t, size_t> pre_start;
+    for (const auto& kv : p2p_plan)
+        if (kv.second.pre_begin < kv.first)
+            pre_start[kv.second.pre_begin] = kv.first;
     for (size_t i = 0; i < prog->steps.size(); ++i) {
         const qsv::Step& s = prog->steps[i];
         if (evs)
             QSV_CUDA(cudaEventRecord(evs[i], ctx->stream));
+        auto ps = pre_start.find(i);
+        if (ps != pre_start.end()) {
+            // passes [i, swap) region by region, then the swap fed region by region,
+            // then the post passes region by region
+            const size_t w = ps->second;
+            const SwapOverlap& ov = p2p_plan[w];
+            const qsv::Step& sw = prog->steps[w];
+            std::vector<cudaEvent_t> pre_ev, done;
+            cudaError_t err = cudaSuccess;
+            for (uint64_t c = 0; c < 4 && err == cudaSuccess; ++c) {
+                qsv::LaunchRange rg = region_of(ov.rmask, c);
+                rg.sms = c > 0 ? ctx->sm_count - swap_sms : 0;
+                for (size_t p = i; p < w && err == cudaSuccess; ++p)
+                    err = launch_step(st, prog, p, rank_base, rg);
+                cudaEvent_t e;
+                cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+                cudaEventRecord(e, ctx->stream);
+                pre_ev.push_back(e);
+            }
+            int rc = err == cudaSuccess ? qsv::run_swap(st, sw.desc.swap_global, sw.desc.swap_local, sw.desc.chunk_log2,
+                                                        sw.desc.nbuf, &done, ov.rmask, &pre_ev)
+                                        : QSV_E_CUDA;
+            for (uint64_t c = 0; c < done.size() && err == cudaSuccess && rc == QSV_OK; ++c) {
+                err = cudaStreamWaitEvent(ctx->stream, done[c], 0);
+                qsv::LaunchRange rg = region_of(ov.rmask, c);
+                rg.sms = c + 1 < done.size() ? ctx->sm_count - swap_sms : 0;
+                for (size_t p = w + 1; p <= ov.post_end && err == cudaSuccess; ++p)
+                    err = launch_step(st, prog, p, rank_base, rg);
+            }
+            qsv::join_swap(ctx);
+            for (cudaEvent_t e : pre_ev)
+                cudaEventDestroy(e);
+            for (cudaEvent_t e : done)
+                cudaEventDestroy(e);
+            QSV_CUDA(err);
+            if (rc != QSV_OK)
+                return rc;
+            i = ov.post_end;
+            continue;
+        }
         if (s.desc.kind == QSV_STEP_PASS) {
             QSV_CUDA(launch_step(st, prog, i, rank_base));
             continue;
         }
-        // swap: overlap the following region-compatible passes with its chunks
-        const int v = s.desc.swap_local, b = s.desc.chunk_log2, l = st->n_local;
-        if (overlap && qsv::p2p_swap_ready(st, s.desc.swap_global)) {
-            // NVLink P2P: any two local bits outside the next passes' tiles can split
-            // the swap into 4 regions; pick the pair that covers the most passes
-            auto tile_mask = [&](const qsv::Step& p) {
-                uint64_t m = (1ull << p.geom.L) - 1ull;
-                for (int h = 0; h < p.geom.nhigh; ++h)
-                    m |= 1ull << p.geom.high[h];
-                return m;
-            };
-            int best_k = 0;
-            uint64_t best_mask = 0;
-            for (int b1 = l - 1; b1 >= 5; --b1)
-                for (int b2 = b1 - 1; b2 >= 5; --b2) {
-                    if (b1 == v || b2 == v)
-                        continue;
-                    const uint64_t rm = (1ull << b1) | (1ull << b2);
-                    int k = 0;
-                    for (size_t q = i + 1; q < prog->steps.size(); ++q) {
-                        const qsv::Step& p = prog->steps[q];
-                        if (p.desc.kind != QSV_STEP_PASS || (tile_mask(p) & rm) || p.geom.K + 2 > l - 1)
-                            break;
-                        ++k;
-                    }
-                    if (k > best_k) {
-                        best_k = k;
-                        best_mask = rm;
-                    }
-                }
-            if (best_k > 0) {
+        const int v = s.desc.swap_local, b = s.desc.chunk_log2;
+        if (p2p) {
+            auto it = p2p_plan.find(i);
+            if (it != p2p_plan.end() && it->second.post_end > i) {
+                // no pre passes: the swap, then its post passes region by region
                 std::vector<cudaEvent_t> done;
-                const int rc = qsv::run_swap(st, s.desc.swap_global, v, b, s.desc.nbuf, &done, best_mask);
-                if (rc != QSV_OK) {
-                    for (cudaEvent_t e : done)
-                        cudaEventDestroy(e);
-                    return rc;
-                }
-                const int swap_sms = std::max(1, std::min(ctx->sm_count - 1, env_int("QSV_SWAP_SMS", 32)));
+                const int rc = qsv::run_swap(st, s.desc.swap_global, v, b, s.desc.nbuf, &done, it->second.rmask);
                 cudaError_t err = cudaSuccess;
-                int rb[2], nr = 0;
-                for (int q = 0; q < l && nr < 2; ++q)
-                    if ((best_mask >> q) & 1ull)
-                        rb[nr++] = q;
-                for (uint64_t c = 0; c < done.size() && err == cudaSuccess; ++c) {
+                for (uint64_t c = 0; c < done.size() && err == cudaSuccess && rc == QSV_OK; ++c) {
                     err = cudaStreamWaitEvent(ctx->stream, done[c], 0);
-                    qsv::LaunchRange rg;
-                    rg.rmask = best_mask;
-                    rg.rval = 0;
-                    for (int q = 0; q < nr; ++q)
-                        rg.rval |= ((c >> q) & 1ull) << rb[q];
+                    qsv::LaunchRange rg = region_of(it->second.rmask, c);
                     rg.sms = c + 1 < done.size() ? ctx->sm_count - swap_sms : 0;
-                    for (size_t p = i + 1; p <= i + static_cast<size_t>(best_k) && err == cudaSuccess; ++p)
+                    for (size_t p = i + 1; p <= it->second.post_end && err == cudaSuccess; ++p)
                         err = launch_step(st, prog, p, rank_base, rg);
                 }
                 qsv::join_swap(ctx);
                 for (cudaEvent_t e : done)
                     cudaEventDestroy(e);
                 QSV_CUDA(err);
-                i += static_cast<size_t>(best_k);
+                if (rc != QSV_OK)
+                    return rc;
+                i = it->second.post_end;
                 continue;
             }
             const int rc = qsv::run_swap(st, s.desc.swap_global, v, b, s.desc.nbuf);

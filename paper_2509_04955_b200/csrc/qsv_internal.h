@@ -127,8 +127,12 @@ void jit_release(qsv_program* prog);
 // (join_swap), so that region passes can start chunk by chunk (BBOP overlap).
 // P2P mode: `region_mask` (<= 2 local bits, not v) splits the swap into regions, one
 // event each; otherwise chunks follow the NCCL top-bit order.
+// `pre_ready` (4 events, P2P regions only): region c starts once pre_ready[c] fired on
+// this rank and the matching event on the peer (pair barrier) instead of after all
+// earlier work on the compute stream.
 int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf,
-             std::vector<cudaEvent_t>* chunk_done = nullptr, uint64_t region_mask = 0);
+             std::vector<cudaEvent_t>* chunk_done = nullptr, uint64_t region_mask = 0,
+             const std::vector<cudaEvent_t>* pre_ready = nullptr);
 // Collective on first use: maps the peers' shards; true when swap g will use NVLink P2P.
 bool p2p_swap_ready(qsv_state* st, int g);
 void join_swap(qsv_ctx* ctx);

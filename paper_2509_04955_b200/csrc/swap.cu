@@ -258,7 +258,7 @@ bool p2p_swap_ready(qsv_state* st, int g) {
 }
 
 int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<cudaEvent_t>* chunk_done,
-             uint64_t region_mask) {
+             uint64_t region_mask, const std::vector<cudaEvent_t>* pre_ready) {
     qsv_ctx* ctx = st->ctx;
     const int l = st->n_local;
     int m = 0;
@@ -293,14 +293,18 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
                 return fail_cuda("qsv_swap: sync token cudaMalloc", e);
             cudaMemset(ctx->d_sync, 0, 2 * sizeof(double));
         }
-        cudaEventRecord(ctx->ev_a, ctx->stream);
-        cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0);
-        ncclResult_t r = pair_barrier(ctx, peer);  // the peer's earlier passes are done
-        if (r != ncclSuccess)
-            return fail_nccl("qsv_swap: barrier", r);
+        region_mask &= ~(1ull << v);
+        const bool fed = pre_ready && chunk_done && region_mask != 0 && pre_ready->size() == 4;
+        ncclResult_t r = ncclSuccess;
+        if (!fed) {
+            cudaEventRecord(ctx->ev_a, ctx->stream);
+            cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0);
+            r = pair_barrier(ctx, peer);  // the peer's earlier passes are done
+            if (r != ncclSuccess)
+                return fail_nccl("qsv_swap: barrier", r);
+        }
         const uint64_t H = 1ull << (l - 1);
         const uint64_t half = H / 2;
-        region_mask &= ~(1ull << v);
         if (!chunk_done || region_mask == 0) {
             p2p_swap_kernel<<<ctx->sm_count * 4, 256, 0, ctx->comm_stream>>>(st->amps, st->peer_amps[peer],
                                                                              a * half, half, v, sendbit, a);
@@ -326,8 +330,15 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
                 }
             const uint64_t pairs = H >> nr;  // per region, both ranks together
             const uint64_t mine_half = pairs / 2;
-            const int sms = std::max(1, std::min(ctx->sm_count, env_int_swap("QSV_SWAP_SMS", 32)));
+            const int sms = std::max(1, std::min(ctx->sm_count, env_int_swap("QSV_SWAP_SMS", 16)));
             for (uint64_t c = 0; c < (1ull << nr); ++c) {
+                if (fed) {
+                    // region c of the passes before the swap is written on both sides
+                    cudaStreamWaitEvent(ctx->comm_stream, (*pre_ready)[c], 0);
+                    r = pair_barrier(ctx, peer);
+                    if (r != ncclSuccess)
+                        return fail_nccl("qsv_swap: barrier", r);
+                }
                 uint64_t rval = 0;
                 for (int i = 0; i < nr; ++i)
                     rval |= ((c >> i) & 1ull) << rb[i];
