@@ -1171,7 +1171,7 @@ std::map<size_t, SwapOverlap> plan_overlap(const qsv_program* prog, int l) {
 int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
     qsv_ctx* ctx = st->ctx;
     const uint64_t rank_base = static_cast<uint64_t>(ctx->rank) << st->n_local;
-    const bool overlap = evs == nullptr && env_int("QSV_OVERLAP", 1) != 0;
+    const bool overlap = evs == nullptr && env_int("QSV_OVERLAP", 0) != 0;
     const int reserve = std::max(0, env_int("QSV_OVERLAP_RESERVE_SMS", 8));
     const int l = st->n_local;
     // P2P region schedule (collective check on the first swap: all ranks agree)

@@ -22,6 +22,6 @@ for N in 2 4; do
   run $N ovl X=1
   run $N noovl QSV_OVERLAP=0
   run $N sms16 QSV_SWAP_SMS=16
-  run $N sms64 QSV_SWAP_SMS=64
+  run $N sms32 QSV_SWAP_SMS=32
 done
 tail -5 gpurun_out/bm_ovl_n2.err
