@@ -57,6 +57,7 @@ class qsim_plan_opts(C.Structure):
         ("rblock_k", C.c_int32),
         ("jit", C.c_int32),
         ("relabel", C.c_int32),
+        ("max_sweeps", C.c_double),
     ]
 
 
@@ -148,11 +149,12 @@ class PlanOptions:
     multi_op_passes: bool = True
     chunk_log2: int = 26
     nbuf: int = 2
-    pass_budget: float = 72.0
+    pass_budget: float = 120.0
     register_blocks: bool = True
     rblock_k: int = 4
     jit: bool = True
     relabel: int = 1  # 0 off, 1 auto (kept when it saves passes), 2 always
+    max_sweeps: float = 8.0
 
     @classmethod
     def default(cls) -> "PlanOptions":
@@ -160,13 +162,13 @@ class PlanOptions:
         load_qsim().qsim_default_opts(C.byref(o))
         return cls(o.tile_k, o.min_low, o.fuse_k, bool(o.fusion), bool(o.multi_op_passes),
                    o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k, bool(o.jit),
-                   int(o.relabel))
+                   int(o.relabel), o.max_sweeps)
 
     def to_c(self) -> qsim_plan_opts:
         return qsim_plan_opts(self.tile_k, self.min_low, self.fuse_k, int(self.fusion),
                               int(self.multi_op_passes), self.chunk_log2, self.nbuf,
                               int(self.register_blocks), float(self.pass_budget), int(self.rblock_k),
-                              int(self.jit), int(self.relabel))
+                              int(self.jit), int(self.relabel), float(self.max_sweeps))
 
 
 class Circuit:

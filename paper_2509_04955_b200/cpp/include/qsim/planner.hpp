@@ -62,7 +62,8 @@ struct PlanOptions {
     int rblock_k = 4;         // register-block width: 3 (8 amplitudes/thread) or 4 (16)
     bool fusion = true;       // DAGC on/off (BASELINE configs[1]: "contraction on vs off")
     bool multi_op_passes = true;  // SMGP on/off: off = one op per pass
-    double pass_budget = 72;  // DP cost units per amplitude allowed in one pass
+    double pass_budget = 120; // DP cost units (DFMA) per amplitude allowed in one pass
+    double max_sweeps = 8;    // SMEM sweeps of the tile per pass (diagonal epilogues count 1/2)
     int n_local = -1;         // local qubits per rank (-1: all, single GPU)
     int chunk_log2 = 26;      // BBOP batch: 2^b amplitudes per swap message; 1 GiB NCCL messages reach ~530 GB/s on NVLink 5 vs ~275 GB/s at 2^22
     int nbuf = 2;             // BBOP buffers B (default 2)

@@ -66,6 +66,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.rblock_k = o->rblock_k;
     p.jit = o->jit != 0;
     p.relabel = o->relabel;
+    p.max_sweeps = o->max_sweeps;
     return p;
 }
 
@@ -120,6 +121,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->rblock_k = p.rblock_k;
     out->jit = p.jit;
     out->relabel = p.relabel;
+    out->max_sweeps = p.max_sweeps;
 }
 
 int qsim_circuit_generate(const char* spec, qsim_circuit** out) {

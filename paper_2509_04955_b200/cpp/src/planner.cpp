@@ -701,6 +701,7 @@ struct Packer {
     std::vector<int> targets;      // physical tile-resident targets of the pass
     std::vector<qsv_op_desc> cur_ops;
     double cur_cost = 0;
+    double cur_sweeps = 0;
     std::size_t cur_bytes = 0;
     // in-pass relabelling lookahead (single rank): the op sequence and the next op index
     const std::vector<Op>* seq = nullptr;
@@ -918,6 +919,7 @@ struct Packer {
         cur_ops.clear();
         targets.clear();
         cur_cost = 0;
+        cur_sweeps = 0;
         cur_bytes = 0;
     }
 
@@ -1047,7 +1049,12 @@ struct Packer {
                 need.push_back(p);
         const double c = op_cost(o);
         const std::size_t b = blob_bytes(o);
+        // SMEM sweeps: every op reads and writes the tile once; a diagonal op right after a
+        // register block rides in its registers (JIT epilogue) and costs about half
+        const bool diag = o.kind == OpKind::Diag || o.kind == OpKind::PhaseProd || o.kind == OpKind::ParPhase;
+        const double sw = diag && !cur_ops.empty() && cur_ops.back().kind == QSV_OP_RBLOCK ? 0.5 : 1.0;
         const bool fits = low_run(need) >= 0 && (cur_ops.empty() || cur_cost + c <= opt.pass_budget) &&
+                          (cur_ops.empty() || cur_sweeps + sw <= opt.max_sweeps) &&
                           cur_bytes + b <= 36 * 1024 && (opt.multi_op_passes || cur_ops.empty());
         if (!fits && !cur_ops.empty()) {
             close_pass();
@@ -1061,6 +1068,7 @@ struct Packer {
         targets = need;
         cur_ops.push_back(to_desc(o));
         cur_cost += c;
+        cur_sweeps += sw;
         cur_bytes += b;
     }
 
