@@ -64,6 +64,7 @@ struct PlanOptions {
     bool multi_op_passes = true;  // SMGP on/off: off = one op per pass
     double pass_budget = 120; // DP cost units (DFMA) per amplitude allowed in one pass
     double max_sweeps = 8;    // SMEM sweeps of the tile per pass (diagonal epilogues count 1/2)
+    bool list_schedule = true;  // single rank: also try a DAG list schedule (ready op that fits first)
     int n_local = -1;         // local qubits per rank (-1: all, single GPU)
     int chunk_log2 = 26;      // BBOP batch: 2^b amplitudes per swap message; 1 GiB NCCL messages reach ~530 GB/s on NVLink 5 vs ~275 GB/s at 2^22
     int nbuf = 2;             // BBOP buffers B (default 2)

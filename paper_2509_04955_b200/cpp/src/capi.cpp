@@ -67,6 +67,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.jit = o->jit != 0;
     p.relabel = o->relabel;
     p.max_sweeps = o->max_sweeps;
+    p.list_schedule = o->list_schedule != 0;
     return p;
 }
 
@@ -122,6 +123,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->jit = p.jit;
     out->relabel = p.relabel;
     out->max_sweeps = p.max_sweeps;
+    out->list_schedule = p.list_schedule;
 }
 
 int qsim_circuit_generate(const char* spec, qsim_circuit** out) {

@@ -1042,6 +1042,20 @@ struct Packer {
         return b;
     }
 
+    // Would `o` join the open pass without closing it?
+    bool fits(const Op& o) const {
+        if (cur_ops.empty())
+            return true;
+        std::vector<int> need = targets;
+        for (int p : tile_needs(o))
+            if (!contains(need, p))
+                need.push_back(p);
+        const bool diag = o.kind == OpKind::Diag || o.kind == OpKind::PhaseProd || o.kind == OpKind::ParPhase;
+        const double sw = diag && cur_ops.back().kind == QSV_OP_RBLOCK ? 0.5 : 1.0;
+        return low_run(need) >= 0 && cur_cost + op_cost(o) <= opt.pass_budget && cur_sweeps + sw <= opt.max_sweeps &&
+               cur_bytes + blob_bytes(o) <= 36 * 1024 && opt.multi_op_passes;
+    }
+
     void add(const Op& o) {
         std::vector<int> need = targets;
         for (int p : tile_needs(o))
@@ -1070,6 +1084,13 @@ struct Packer {
         cur_cost += c;
         cur_sweeps += sw;
         cur_bytes += b;
+    }
+
+    // Swap two logical qubits (one global, one local).  Positions are read after the
+    // open pass is closed, since closing it may relabel the tile.
+    void swap_logical(int qg, int qv) {
+        close_pass();
+        swap(pos[qg], pos[qv]);
     }
 
     void swap(int g_phys, int v_phys) {
@@ -1108,7 +1129,9 @@ static double plan_time_model(const Plan& p) {
     double t = 0;
     for (const qsv_step_desc& s : p.steps) {
         if (s.kind != QSV_STEP_PASS) {
-            t += 1.0;
+            // a swap moves 16 B per amplitude pair over NVLink (~685 GB/s P2P) against a
+            // pass's 32 B per amplitude over HBM: ~2.4 pass-equivalents
+            t += 2.4;
             continue;
         }
         const int L = s.tile_k - s.nhigh;
@@ -1122,16 +1145,85 @@ static double plan_time_model(const Plan& p) {
 }
 
 // Packs the final op list into passes (SMGP) and, across ranks, BBOP swaps.
-static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOptions& opt, Plan plan) {
+// A multi-rank schedule: op indices (>= 0) and swaps of logical qubits (-1 - i into swaps).
+struct Schedule {
+    std::vector<int> order;
+    std::vector<std::pair<int, int>> swaps;  // (logical global qubit, logical victim)
+};
+
+static void finish_plan(const Circuit& c, const PlanOptions& opt, Packer& pk, Plan& plan);
+
+// Replays a multi-rank schedule with tile relabelling (lookahead over the scheduled order).
+static Plan replay_schedule(const Circuit& c, const std::vector<Op>& ops, const Schedule& sch,
+                            const PlanOptions& opt, Plan plan) {
+    Packer pk(opt, c.n, plan.n_local, plan);
+    std::vector<Op> seq;
+    for (int e : sch.order)
+        if (e >= 0)
+            seq.push_back(ops[e]);
+    pk.seq = &seq;
+    std::size_t cur = 0;
+    for (int e : sch.order) {
+        if (e >= 0) {
+            pk.cursor = cur++;
+            pk.add(ops[e]);
+        } else {
+            pk.cursor = cur;
+            const auto& sw = sch.swaps[static_cast<std::size_t>(-1 - e)];
+            pk.swap_logical(sw.first, sw.second);
+        }
+    }
+    pk.cursor = seq.size();
+    finish_plan(c, opt, pk, plan);
+    return plan;
+}
+
+static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOptions& opt, Plan plan,
+                     Schedule* sched = nullptr) {
     Packer pk(opt, c.n, plan.n_local, plan);
     const int nops = static_cast<int>(ops.size());
-    if (plan.n_local == c.n) {
+    if (plan.n_local == c.n && !sched) {
         pk.seq = &ops;
         for (std::size_t i = 0; i < ops.size(); ++i) {
             pk.cursor = i;
             pk.add(ops[i]);
         }
         pk.cursor = ops.size();
+    } else if (plan.n_local == c.n) {
+        // single rank, list-scheduled: the earliest ready op that fits the open pass
+        // (commuting ops move up into it); the order is recorded for a relabel replay
+        std::vector<int> npred(nops, 0);
+        std::vector<std::vector<int>> succ(nops);
+        std::vector<int> last(static_cast<std::size_t>(c.n), -1);
+        for (int i = 0; i < nops; ++i) {
+            std::vector<int> preds;
+            for (int q : footprint(ops[i])) {
+                if (last[q] >= 0 && !contains(preds, last[q]))
+                    preds.push_back(last[q]);
+                last[q] = i;
+            }
+            npred[i] = static_cast<int>(preds.size());
+            for (int p : preds)
+                succ[p].push_back(i);
+        }
+        std::vector<int> ready;
+        for (int i = 0; i < nops; ++i)
+            if (npred[i] == 0)
+                ready.push_back(i);
+        for (int done = 0; done < nops; ++done) {
+            int pick = -1;
+            for (int i : ready)
+                if ((pick < 0 || i < pick) && pk.fits(ops[i]))
+                    pick = i;
+            if (pick < 0)
+                pick = *std::min_element(ready.begin(), ready.end());
+            ready.erase(std::find(ready.begin(), ready.end(), pick));
+            sched->order.push_back(pick);
+            pk.add(ops[pick]);
+            for (int sI : succ[pick])
+                if (--npred[sI] == 0)
+                    ready.push_back(sI);
+        }
     } else {
         // Local-first list scheduling over the dependency DAG (multi-GPU): run
         // every ready op whose tile qubits are all local; only when none is ready
@@ -1199,10 +1291,16 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
                     }
                     if (best < 0)
                         throw std::logic_error("planner: no swap victim available");
-                    pk.swap(pk.pos[q], pk.pos[best]);
+                    if (sched) {
+                        sched->swaps.emplace_back(q, best);
+                        sched->order.push_back(-static_cast<int>(sched->swaps.size()));
+                    }
+                    pk.swap_logical(q, best);
                 }
             }
             ready.erase(std::find(ready.begin(), ready.end(), pick));
+            if (sched)
+                sched->order.push_back(pick);
             pk.add(ops[pick]);
             for (int q : local_needs(ops[pick]))
                 --remaining[q];
@@ -1212,9 +1310,28 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
                     ready.push_back(sI);
         }
     }
+    finish_plan(c, opt, pk, plan);
+    return plan;
+}
+
+// Closes the last pass, restores the logical qubit order (relabel passes, then swaps
+// and local slot swaps) so the final state is in the standard layout.
+static void finish_plan(const Circuit& c, const PlanOptions& opt, Packer& pk, Plan& plan) {
     pk.close_pass();
+    // 1. global slots first: one swap brings each global slot's own qubit home
+    for (int G = plan.n_local; G < c.n; ++G) {
+        if (pk.pos[G] == G)
+            continue;
+        int at = pk.pos[G];
+        if (at >= plan.n_local) {  // it sits in another global slot: route through a local slot
+            const int t = plan.n_local - 1;
+            pk.swap(at, t);
+            at = t;
+        }
+        pk.swap(G, at);
+    }
+    // 2. local slots: pure relabel passes (each fixes the cycles its tile holds)
     if (pk.seq != nullptr && opt.relabel) {
-        // pure relabel passes until every qubit is home (each fixes the cycles it can)
         if (std::getenv("QSV_PLAN_DEBUG"))
             std::fprintf(stderr, "plan: before restore passes=%zu misplaced=%d\n", plan.stats.passes, pk.misplaced_local());
         for (int guard = 0; guard < 64 && pk.misplaced_local() > 0; ++guard) {
@@ -1261,7 +1378,6 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
             pk.swap(a, t);
         }
     }
-    return plan;
 }
 
 Plan make_plan(const Circuit& c, const PlanOptions& opt) {
@@ -1312,18 +1428,31 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     PlanOptions o_plain = opt;
     o_plain.relabel = 0;
     const bool single = plan.n_local == c.n;
-    Plan best = (opt.relabel == 2 && single) ? pack_ops(c, ops, opt, plan) : pack_ops(c, ops, o_plain, plan);
-    if (opt.relabel == 1 && single) {
-        // relabelled plans keep >= 1 KB HBM runs (min_low 6): 512-B runs cost ~16 %
-        PlanOptions o_rl = opt;
-        o_rl.min_low = std::max(opt.min_low, 6);
+    Schedule sch;
+    Plan best = (opt.relabel == 2 && single) ? pack_ops(c, ops, opt, plan)
+                                             : pack_ops(c, ops, o_plain, plan, single ? nullptr : &sch);
+    if (!single && opt.relabel == 2)
+        best = replay_schedule(c, ops, sch, opt, plan);
+    auto consider = [&](auto&& make) {
         try {
-            Plan alt = pack_ops(c, ops, o_rl, plan);
+            Plan alt = make();
             if (plan_time_model(alt) < plan_time_model(best))
                 best = std::move(alt);
         } catch (const std::logic_error&) {
             // the blocks were formed for the caller's low run; a longer one may not fit
         }
+    };
+    Schedule lsch;
+    if (single && opt.multi_op_passes && opt.list_schedule && opt.relabel != 2)  // list-scheduled order
+        consider([&] { return pack_ops(c, ops, o_plain, plan, &lsch); });
+    if (opt.relabel == 1) {
+        // relabelled plans keep >= 1 KB HBM runs (min_low 6): 512-B runs cost ~16 %
+        PlanOptions o_rl = opt;
+        o_rl.min_low = std::max(opt.min_low, 6);
+        // multi-rank: the list schedule (swaps included) is kept, only packing changes
+        consider([&] { return single ? pack_ops(c, ops, o_rl, plan) : replay_schedule(c, ops, sch, o_rl, plan); });
+        if (!lsch.order.empty())
+            consider([&] { return replay_schedule(c, ops, lsch, o_rl, plan); });
     }
     best.fused = std::move(ops);
     return best;

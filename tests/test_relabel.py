@@ -51,3 +51,23 @@ def test_relabel_rejects_non_permutation():
     steps[i].relabel[1] = steps[i].relabel[0]
     rc = E.validate(steps, ops, prims, pool, c.n, c.n, 0)
     assert rc != 0
+
+
+@pytest.mark.parametrize("spec", CASES)
+@pytest.mark.parametrize("kw", [dict(), dict(tile_k=7, min_low=3), dict(tile_k=8, min_low=4, pass_budget=200.0)])
+def test_default_plans_match_oracle(spec, kw):
+    """The auto planner (list schedule x relabel, picked by plan_time_model) executed
+    step by step by the emulator equals the oracle."""
+    c = pkg.Circuit.generate(spec)
+    steps, ops, prims, pool = E.export_plan(c, pkg.PlanOptions(**kw), c.n)
+    a = rand_state(c.n, 5)
+    psi = E.run_program(a.copy(), steps, ops, prims, pool, 0, c.n, None)
+    assert np.abs(psi - O.run_local(c, a)).max() < 1e-10
+
+
+def test_list_schedule_never_worse():
+    for spec in ("random:14:10:2", "hea:13:4:4", "qaoa:12:2:1"):
+        c = pkg.Circuit.generate(spec)
+        on = c.plan(pkg.PlanOptions(tile_k=8))["passes"]
+        off = c.plan(pkg.PlanOptions(tile_k=8, list_schedule=False, relabel=0))["passes"]
+        assert on <= off
