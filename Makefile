@@ -18,7 +18,7 @@ HDRS     := $(wildcard include/*.h) $(wildcard $(PKG)/csrc/*.h) $(wildcard $(PKG
 TESTS_CPP:= $(wildcard tests/cpp/*.cpp)
 TEST_BIN := $(patsubst tests/cpp/%.cpp,build/tests/%,$(TESTS_CPP))
 
-all: $(LIB)/libqsv.so $(LIB)/libqsim.so oracle/liboracle.so ref tests-cpp
+all: $(LIB)/libqsv.so $(LIB)/libqsim.so $(LIB)/qsv oracle/liboracle.so ref tests-cpp
 
 build/cu/%.o: $(PKG)/csrc/%.cu $(HDRS) build/jit_src.inc
 	@mkdir -p $(dir $@)
@@ -41,6 +41,10 @@ build/cpp/%.o: $(PKG)/cpp/src/%.cpp $(HDRS)
 $(LIB)/libqsim.so: $(CPP_OBJ) $(LIB)/libqsv.so
 	$(CXX) -shared -o $@ $(CPP_OBJ) -L$(LIB) -lqsv -Wl,-rpath,'$$ORIGIN' -lpthread
 
+# `qsv run ...` report driver
+$(LIB)/qsv: $(PKG)/cpp/tools/qsv.cpp $(LIB)/libqsim.so $(HDRS)
+	$(CXX) $(CXXFLAGS) $< -o $@ -L$(LIB) -lqsim -lqsv -Wl,-rpath,'$$ORIGIN'
+
 oracle/liboracle.so: oracle/oracle.cpp oracle/oracle.h
 	$(CXX) -std=c++20 -O3 -march=x86-64-v3 -fPIC -shared -Wall -Wextra $< -o $@ -lpthread
 
@@ -54,6 +58,6 @@ build/tests/%: tests/cpp/%.cpp $(LIB)/libqsim.so $(HDRS)
 tests-cpp: $(TEST_BIN)
 
 clean:
-	rm -rf build $(LIB)/*.so oracle/liboracle.so oracle/_ref
+	rm -rf build $(LIB)/*.so $(LIB)/qsv oracle/liboracle.so oracle/_ref
 
 .PHONY: all ref clean tests-cpp
