@@ -169,27 +169,17 @@ def run_reference_arm(args):
 def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, local, barrier, dist):
     """End-to-end through the public engine API with host buffers: every step uploads
     its input state from pinned host memory, runs the circuit and downloads the final
-    state.  Two engines (two HBM states, two streams) alternate so that the H2D of
-    step k+1 and the D2H of step k-1 overlap the run of step k (full-duplex PCIe);
-    falls back to one engine (strictly sequential copies) when a second state does
-    not fit."""
+    state.  Up to three engines (three HBM states, three streams) take steps in turn and
+    are staggered with stream events so that uploads follow uploads, runs follow runs and
+    downloads follow downloads: in steady state the H2D of step k+1, the run of step k and
+    the D2H of step k-1 proceed together (full-duplex PCIe), the way a serving loop would
+    stream circuits.  Falls back to fewer engines when states do not fit (one engine =
+    strictly sequential copies)."""
     N = 1 << n_local
     L = pkg.load_qsim()
-    bufs = [C.c_void_p() for _ in range(3)]
-    for h in bufs:
-        if qsv.qsv_host_alloc(C.c_size_t(16 * N), C.byref(h)) != 0:
-            for g in bufs:
-                if g.value:
-                    qsv.qsv_host_free(g)
-            return None
-    src = np.ctypeslib.as_array(C.cast(bufs[0], C.POINTER(C.c_double)), shape=(2 * N,))
-    src[:] = 0.0
-    if rank == 0:
-        src[0] = 1.0  # |0...0>: the host-side input of every step
-    din = C.cast(bufs[0], C.POINTER(C.c_double))
-    douts = [C.cast(bufs[1], C.POINTER(C.c_double)), C.cast(bufs[2], C.POINTER(C.c_double))]
+    want = 1 if args.e2e_sequential else 3
     engines = [eng]
-    if not args.e2e_sequential:
+    while len(engines) < want:
         try:
             cid = None
             if world > 1:
@@ -200,22 +190,60 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
                 cid = obj[0]
             engines.append(pkg.Engine(circ, opts, device=local if world > 1 else 0, rank=rank, nranks=world,
                                       comm_id=cid))
-        except Exception as exc:  # second 2^n state does not fit: sequential copies
-            print(f"bench: e2e falls back to one engine ({exc})", file=sys.stderr)
+        except Exception as exc:  # no room for another 2^n state
+            print(f"bench: e2e uses {len(engines)} engine(s) ({exc})", file=sys.stderr)
+            break
     ne = len(engines)
+    bufs = [C.c_void_p() for _ in range(1 + ne)]
+    for h in bufs:
+        if qsv.qsv_host_alloc(C.c_size_t(16 * N), C.byref(h)) != 0:
+            for g in bufs:
+                if g.value:
+                    qsv.qsv_host_free(g)
+            for e in engines[1:]:
+                e.close()
+            return None
+    src = np.ctypeslib.as_array(C.cast(bufs[0], C.POINTER(C.c_double)), shape=(2 * N,))
+    src[:] = 0.0
+    if rank == 0:
+        src[0] = 1.0  # |0...0>: the host-side input of every step
+    din = C.cast(bufs[0], C.POINTER(C.c_double))
+    douts = [C.cast(bufs[1 + i], C.POINTER(C.c_double)) for i in range(ne)]
+    streams = [C.c_void_p(e.stream()) for e in engines]
+    evs = {}
+
+    def event(kind, k):
+        ev = C.c_void_p()
+        qsv.qsv_event_create(C.byref(ev))
+        evs[(kind, k)] = ev
+        return ev
 
     def step(k):
-        e = engines[k % ne]
+        i = k % ne
+        e, s = engines[i], streams[i]
+        if ne > 1 and ("up", k - 1) in evs:
+            qsv.qsv_stream_wait_event(s, evs[("up", k - 1)])
         L.qsim_engine_upload(e._h, din, C.c_uint64(0), C.c_uint64(N))
+        if ne > 1:
+            qsv.qsv_event_record(event("up", k), s)
+            if ("run", k - 1) in evs:
+                qsv.qsv_stream_wait_event(s, evs[("run", k - 1)])
         e.run()
         if ne == 1:
             L.qsim_engine_download(e._h, douts[0], C.c_uint64(0), C.c_uint64(N))
-        else:
-            L.qsim_engine_download_async(e._h, douts[k % ne], C.c_uint64(0), C.c_uint64(N))
+            return
+        qsv.qsv_event_record(event("run", k), s)
+        if ("down", k - 1) in evs:
+            qsv.qsv_stream_wait_event(s, evs[("down", k - 1)])
+        L.qsim_engine_download_async(e._h, douts[i], C.c_uint64(0), C.c_uint64(N))
+        qsv.qsv_event_record(event("down", k), s)
 
     def drain():
         for e in engines:
             e.sync()
+        for ev in evs.values():
+            qsv.qsv_event_destroy(ev)
+        evs.clear()
 
     for k in range(ne):  # warm-up: each engine once (graph capture, attributes)
         step(k)
@@ -239,9 +267,9 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
         e.close()
     for h in bufs:
         qsv.qsv_host_free(h)
-    api = ("qsim_engine_upload -> qsim_engine_run -> qsim_engine_download_async on 2 engines "
-           "(ping-pong: H2D(k+1) | run(k) | D2H(k-1) overlap; pinned host buffers, full state in and out)"
-           if ne == 2 else
+    api = (f"qsim_engine_upload -> qsim_engine_run -> qsim_engine_download_async on {ne} engines, staggered by "
+           "stream events (H2D(k+1) | run(k) | D2H(k-1)); pinned host buffers, full state in and out"
+           if ne > 1 else
            "qsim_engine_upload -> qsim_engine_run -> qsim_engine_download (pinned host buffers, full state in and out)")
     return {"value": gates / e2e_s, "unit": "gates/s", "h2d_bytes_per_step": 16 * N * world,
             "d2h_bytes_per_step": 16 * N * world, "seconds_per_step": e2e_s, "engines": ne,

@@ -97,6 +97,12 @@ int qsv_state_download(qsv_state* st, double* host, uint64_t offset, uint64_t co
  * context stream; call qsv_sync before reading `host`.  With pinned host memory it
  * overlaps other contexts' work (used for pipelined end-to-end streaming). */
 int qsv_state_download_async(qsv_state* st, double* host, uint64_t offset, uint64_t count);
+/* Stream events between contexts (e.g. staggering several engines' copies and runs):
+ * `stream` is a handle from qsv_ctx_stream / qsim_engine_stream. */
+int qsv_event_create(void** ev);
+int qsv_event_destroy(void* ev);
+int qsv_event_record(void* ev, void* stream);
+int qsv_stream_wait_event(void* stream, void* ev);
 /* Raw device pointer of the shard (double2*), for interop/tests. */
 int qsv_state_device_ptr(qsv_state* st, void** ptr);
 /* Pinned host buffers for the upload/download paths. */

@@ -399,6 +399,32 @@ extern "C" int qsv_state_download_async(qsv_state* st, double* host, uint64_t of
     return QSV_OK;
 }
 
+extern "C" int qsv_event_create(void** ev) {
+    QSV_REQUIRE(ev != nullptr, "qsv_event_create: null output");
+    cudaEvent_t e;
+    QSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    *ev = e;
+    return QSV_OK;
+}
+
+extern "C" int qsv_event_destroy(void* ev) {
+    if (ev)
+        QSV_CUDA(cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+    return QSV_OK;
+}
+
+extern "C" int qsv_event_record(void* ev, void* stream) {
+    QSV_REQUIRE(ev != nullptr, "qsv_event_record: null event");
+    QSV_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)));
+    return QSV_OK;
+}
+
+extern "C" int qsv_stream_wait_event(void* stream, void* ev) {
+    QSV_REQUIRE(ev != nullptr, "qsv_stream_wait_event: null event");
+    QSV_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev), 0));
+    return QSV_OK;
+}
+
 extern "C" int qsv_state_device_ptr(qsv_state* st, void** ptr) {
     QSV_REQUIRE(st != nullptr && ptr != nullptr, "qsv_state_device_ptr: null argument");
     *ptr = st->amps;
