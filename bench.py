@@ -209,7 +209,7 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
         src[0] = 1.0  # |0...0>: the host-side input of every step
     din = C.cast(bufs[0], C.POINTER(C.c_double))
     douts = [C.cast(bufs[1 + i], C.POINTER(C.c_double)) for i in range(ne)]
-    streams = [C.c_void_p(e.stream()) for e in engines]
+    streams = [C.c_void_p(e.stream) for e in engines]
     evs = {}
 
     def event(kind, k):

@@ -49,6 +49,7 @@ typedef struct qsim_plan_opts {
     int32_t relabel;          /* tile-qubit relabel at pass ends: 0 off, 1 auto, 2 always */
     double max_sweeps;        /* SMEM sweeps of the tile per pass                */
     int32_t list_schedule;    /* single rank: also try a DAG list schedule       */
+    int32_t jit_max_kernels;  /* distinct specialised pass kernels compiled at most */
 } qsim_plan_opts;
 
 typedef struct qsim_plan_stats {

@@ -59,6 +59,7 @@ class qsim_plan_opts(C.Structure):
         ("relabel", C.c_int32),
         ("max_sweeps", C.c_double),
         ("list_schedule", C.c_int32),
+        ("jit_max_kernels", C.c_int32),
     ]
 
 
@@ -157,6 +158,7 @@ class PlanOptions:
     relabel: int = 1  # 0 off, 1 auto (kept when it saves passes), 2 always
     max_sweeps: float = 8.0
     list_schedule: bool = True
+    jit_max_kernels: int = 2048
 
     @classmethod
     def default(cls) -> "PlanOptions":
@@ -164,14 +166,14 @@ class PlanOptions:
         load_qsim().qsim_default_opts(C.byref(o))
         return cls(o.tile_k, o.min_low, o.fuse_k, bool(o.fusion), bool(o.multi_op_passes),
                    o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k, bool(o.jit),
-                   int(o.relabel), o.max_sweeps, bool(o.list_schedule))
+                   int(o.relabel), o.max_sweeps, bool(o.list_schedule), o.jit_max_kernels)
 
     def to_c(self) -> qsim_plan_opts:
         return qsim_plan_opts(self.tile_k, self.min_low, self.fuse_k, int(self.fusion),
                               int(self.multi_op_passes), self.chunk_log2, self.nbuf,
                               int(self.register_blocks), float(self.pass_budget), int(self.rblock_k),
                               int(self.jit), int(self.relabel), float(self.max_sweeps),
-                              int(self.list_schedule))
+                              int(self.list_schedule), int(self.jit_max_kernels))
 
 
 class Circuit:

@@ -68,6 +68,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.relabel = o->relabel;
     p.max_sweeps = o->max_sweeps;
     p.list_schedule = o->list_schedule != 0;
+    p.jit_max_kernels = o->jit_max_kernels;
     return p;
 }
 
@@ -124,6 +125,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->relabel = p.relabel;
     out->max_sweeps = p.max_sweeps;
     out->list_schedule = p.list_schedule;
+    out->jit_max_kernels = p.jit_max_kernels;
 }
 
 int qsim_circuit_generate(const char* spec, qsim_circuit** out) {
