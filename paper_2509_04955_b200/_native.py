@@ -158,7 +158,7 @@ class PlanOptions:
     relabel: int = 1  # 0 off, 1 auto (kept when it saves passes), 2 always
     max_sweeps: float = 8.0
     list_schedule: bool = True
-    jit_max_kernels: int = 2048
+    jit_max_kernels: int = 8192
 
     @classmethod
     def default(cls) -> "PlanOptions":

@@ -69,7 +69,7 @@ struct PlanOptions {
     int chunk_log2 = 26;      // BBOP batch: 2^b amplitudes per swap message; 1 GiB NCCL messages reach ~530 GB/s on NVLink 5 vs ~275 GB/s at 2^22
     int nbuf = 2;             // BBOP buffers B (default 2)
     bool jit = true;          // NVRTC-specialised pass kernels (falls back to the interpreter kernel)
-    int jit_max_kernels = 2048; // distinct pass structures compiled at most (the rest interpreted)
+    int jit_max_kernels = 8192; // distinct pass structures compiled at most (the rest interpreted)
     int relabel = 1;          // tile-qubit relabelling at pass ends: 0 off, 1 auto (kept when it
                               // saves passes), 2 always (tests)
 };

@@ -115,7 +115,17 @@ const Driver& driver() {
 }
 
 // ------------------------------------------------------------------ codegen
-int threads_for_k(int K) { return K >= 12 ? 256 : (K >= 8 ? 128 : (K >= 6 ? 64 : 32)); }
+// Split register blocks (two threads per 16-member group, 256 threads for 11-qubit
+// tiles); QSV_JIT_SPLIT=0 keeps one thread per group.
+bool split_blocks() {
+    const char* e = std::getenv("QSV_JIT_SPLIT");
+    return !(e && e[0] == '0');
+}
+int threads_for_k(int K) {
+    if (K == 11 && split_blocks())
+        return 256;
+    return K >= 12 ? 256 : (K >= 8 ? 128 : (K >= 6 ? 64 : 32));
+}
 
 std::string u32(uint32_t x) {
     std::ostringstream o;
@@ -135,7 +145,7 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
     const int NT = threads_for_k(K);
     const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
     std::ostringstream o;
-    minb = K >= 12 ? 1 : 3;
+    minb = K >= 12 ? 1 : (NT >= 256 ? 2 : 3);
     for (int i = 0; i < s.nops; ++i) {
         const TileOp& op = ops[i];
         const std::string opref = "*reinterpret_cast<const qsv::TileOp*>(blob + " +
@@ -232,6 +242,97 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
             uint32_t rot_any = 0;
             for (int l = 0; l < 8; ++l)
                 rot_any |= (op.rot_tab >> (4 * l)) & 15u;
+            const DevPrim* prs = reinterpret_cast<const DevPrim*>(blob + op.prim_byte);
+            if (KB == 4 && NT == 256 && (1 << (K - __builtin_popcount(op.fmask))) * 2 == NT) {
+                // ---- split block: body over 8 registers per thread, re-split on demand
+                auto crosses = [&](const DevPrim& q, int S) {
+                    switch (q.kind) {
+                    case QSV_PRIM_U1: case QSV_PRIM_U1R: case QSV_PRIM_U1I: return q.a == S;
+                    case QSV_PRIM_U2: return q.a == S || q.b == S;
+                    case QSV_PRIM_CX: return q.b == S;
+                    default: return false;
+                    }
+                };
+                auto next_cross = [&](int S, int from) {
+                    for (int p = from; p < op.nprim; ++p)
+                        if (crosses(prs[p], S))
+                            return p;
+                    return op.nprim + 1;
+                };
+                int S = 0;
+                for (int c = 1; c < 4; ++c)
+                    if (next_cross(c, 0) > next_cross(S, 0))
+                        S = c;
+                const int S0 = S;
+                std::ostringstream body;
+                auto loc = [&](int slot) { return slot < S ? slot : slot - 1; };
+                for (int p = 0; p < op.nprim; ++p) {
+                    const DevPrim& q = prs[p];
+                    if (crosses(q, S)) {
+                        int best = -1;
+                        for (int c = 0; c < 4; ++c) {
+                            if (c == S || c == q.a || (q.kind == QSV_PRIM_U2 || q.kind == QSV_PRIM_CX ? c == q.b : false))
+                                continue;
+                            if (best < 0 || next_cross(c, p) > next_cross(best, p))
+                                best = c;
+                        }
+                        body << "    qsv::rb_resplit<" << S << ", " << best << ">(v, h);\n";
+                        S = best;
+                    }
+                    const std::string mat = "reinterpret_cast<const double2*>(blob + " + std::to_string(q.data_byte) + ")";
+                    const bool ra = (rot_any >> q.a) & 1u, rb = (rot_any >> q.b) & 1u;
+                    switch (q.kind) {
+                    case QSV_PRIM_U1:
+                    case QSV_PRIM_U1R:
+                    case QSV_PRIM_U1I: {
+                        const char* fn = q.kind == QSV_PRIM_U1 ? "rb_u1" : (q.kind == QSV_PRIM_U1R ? "rb_u1r" : "rb_u1i");
+                        body << "    qsv::" << fn << "<8, " << loc(q.a) << ">(v, " << mat;
+                        if (ra)
+                            body << " + 4u * ((r >> " << int(q.a) << ") & 1u)";
+                        body << ");\n";
+                        break;
+                    }
+                    case QSV_PRIM_U2:
+                        body << "    qsv::rb_u2<8, " << loc(q.a) << ", " << loc(q.b) << ">(v, " << mat;
+                        if (ra || rb)
+                            body << " + 16u * (((r >> " << int(q.a) << ") & 1u) | (((r >> " << int(q.b) << ") & 1u) << 1))";
+                        body << ");\n";
+                        break;
+                    case QSV_PRIM_CX:
+                        if (q.a == S) {
+                            body << "    if (h != " << (ra ? "((r >> " + std::to_string(q.a) + ") & 1u)" : std::string("0u"))
+                                 << ") qsv::rb_flip<" << loc(q.b) << ">(v);\n";
+                        } else if (ra) {
+                            body << "    qsv::rb_cx<8, " << loc(q.a) << ", " << loc(q.b) << ">(v, (r & " << ((1 << S) - 1)
+                                 << "u) | ((r >> " << (S + 1) << ") << " << S << "));\n";
+                        } else {
+                            body << "    qsv::rb_cx_plain<8, " << loc(q.a) << ", " << loc(q.b) << ">(v);\n";
+                        }
+                        break;
+                    default:
+                        body << "    qsv::rb_diag_split<" << S << ">(v, " << mat << ", " << (rot_any ? "r" : "0u") << ", h);\n";
+                        break;
+                    }
+                }
+                o << "  qsv::jit_rblock_split<" << K << ", " << NT << ", " << u32(op.fmask) << ", " << u32(op.tctrl)
+                  << ", " << u32(m[0]) << ", " << u32(m[1]) << ", " << u32(m[2]) << ", " << u32(m[3]) << ", "
+                  << u32(op.rot_tab) << ", " << S0 << ", " << S << ">(tile, [&](double2 (&v)[8], uint32_t r, uint32_t h) {\n";
+                if (last > i) {
+                    std::string call = o.str();
+                    const std::string head = "  qsv::jit_rblock_split<";
+                    const size_t at = call.rfind(head);
+                    o.str("");
+                    o << call.substr(0, at) << pre.str() << call.substr(at);
+                }
+                o << "    (void)r; (void)h;\n" << body.str();
+                if (last > i) {
+                    o << "  }, [&](double2& a, uint32_t idx) {\n    (void)idx;\n" << epi.str() << "  });\n";
+                    i = last;
+                } else {
+                    o << "  }, qsv::NoEpi{});\n";
+                }
+                break;
+            }
             o << "  qsv::jit_rblock<" << K << ", " << NT << ", " << KB << ", " << u32(op.fmask) << ", "
               << u32(op.tctrl) << ", " << u32(m[0]) << ", " << u32(m[1]) << ", " << u32(m[2]) << ", " << u32(m[3])
               << ", " << u32(op.rot_tab) << ">(tile, [&](double2 (&v)[" << NV << "], uint32_t r) {\n";

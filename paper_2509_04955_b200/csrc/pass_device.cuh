@@ -788,6 +788,110 @@ __device__ __forceinline__ void rb_cx_plain(double2 (&v)[NV]) {
     }
 }
 
+// ------------------------------------------------ split register blocks (JIT)
+// A 16-member register group held by a lane pair (lane, lane ^ 16): the lane with
+// h = lane >> 4 holds the 8 members whose bit on the split slot S equals h, at local
+// index = member index with bit S removed.  Twice the threads per group means twice
+// the warps per SM for the same registers per group (latency hiding for DFMA-heavy
+// passes).  Primitives not crossing the split run on the 8 local registers; before one
+// that does, the pair re-splits on another slot through four 16-B shuffles.
+__host__ __device__ constexpr int rb_compress(int j, int S) {  // drop bit S of a 4-bit index
+    return (j & ((1 << S) - 1)) | ((j >> (S + 1)) << S);
+}
+__host__ __device__ constexpr int rb_expand(int x, int S, int bit) {  // insert `bit` at S
+    return (x & ((1 << S) - 1)) | (bit << S) | ((x >> S) << (S + 1));
+}
+// the 4-bit member index with bit SO = so, bit SN = sn and the other two slots = q
+__host__ __device__ constexpr int rb_member(int SO, int SN, int so, int sn, int q) {
+    int j = 0, k = 0;
+    for (int b = 0; b < 4; ++b) {
+        if (b == SO)
+            j |= so << b;
+        else if (b == SN)
+            j |= sn << b;
+        else
+            j |= ((q >> k++) & 1) << b;
+    }
+    return j;
+}
+
+__device__ __forceinline__ double2 shfl_xor16(double2 a) {
+    double2 r;
+    r.x = __shfl_xor_sync(0xffffffffu, a.x, 16);
+    r.y = __shfl_xor_sync(0xffffffffu, a.y, 16);
+    return r;
+}
+
+template <int SO, int SN>
+__device__ __forceinline__ void rb_resplit(double2 (&v)[8], uint32_t h) {
+    double2 nv[8];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int x0 = rb_compress(rb_member(SO, SN, 0, 0, q), SO);  // s_new = 0 (s_old = h)
+        const int x1 = rb_compress(rb_member(SO, SN, 0, 1, q), SO);  // s_new = 1
+        const double2 keep = h ? v[x1] : v[x0];
+        const double2 send = h ? v[x0] : v[x1];
+        const double2 recv = shfl_xor16(send);
+        const int y0 = rb_compress(rb_member(SO, SN, 0, 0, q), SN);  // s_old = 0
+        const int y1 = rb_compress(rb_member(SO, SN, 1, 0, q), SN);  // s_old = 1
+        nv[y0] = h ? recv : keep;
+        nv[y1] = h ? keep : recv;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        v[i] = nv[i];
+}
+
+template <int T>  // swap the register pairs differing in local bit T (CX whose control is the split slot)
+__device__ __forceinline__ void rb_flip(double2 (&v)[8]) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if ((j >> T) & 1)
+            continue;
+        const double2 t = v[j];
+        v[j] = v[j | (1 << T)];
+        v[j | (1 << T)] = t;
+    }
+}
+
+template <int S>  // 16-entry diagonal over the full member index (split on S)
+__device__ __forceinline__ void rb_diag_split(double2 (&v)[8], const double2* D, uint32_t r, uint32_t h) {
+#pragma unroll
+    for (int x = 0; x < 8; ++x)
+        v[x] = cmul(D[static_cast<uint32_t>(rb_expand(x, S, 0)) ^ (h << S) ^ r], v[x]);
+}
+
+template <int K, int NT, uint32_t F, uint32_t TCTRL, uint32_t M0, uint32_t M1, uint32_t M2, uint32_t M3,
+          uint32_t ROT, int S0, int S1, typename Body, typename Epi>
+__device__ __forceinline__ void jit_rblock_split(double2* tile, Body&& body, Epi&& epi) {
+    static_assert((1 << (K - cpopc(F))) * 2 == NT, "split blocks need exactly two threads per group");
+    constexpr uint32_t M[4] = {M0, M1, M2, M3};
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t h = lane >> 4;
+    const uint32_t g = ((threadIdx.x >> 5) << 4) | (lane & 15u);
+    const uint32_t r = ROT ? ((ROT >> (4 * (lane & 7))) & 15u) : 0u;
+    const uint32_t offr = ((r & 1u) ? M0 : 0u) | ((r & 2u) ? M1 : 0u) | ((r & 4u) ? M2 : 0u) | ((r & 8u) ? M3 : 0u);
+    const uint32_t base = cdeposit(g, F) | TCTRL | offr;
+    double2 v[8];
+    {
+        const uint32_t b0 = base ^ (h ? M[S0] : 0u);
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+            const int j = rb_expand(x, S0, 0);
+            v[x] = tile[b0 ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))];
+        }
+    }
+    body(v, r, h);
+    const uint32_t b1 = base ^ (h ? M[S1] : 0u);
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+        const int j = rb_expand(x, S1, 0);
+        const uint32_t idx = b1 ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u));
+        epi(v[x], idx);
+        tile[idx] = v[x];
+    }
+}
+
 // Register block with every structural quantity a compile-time constant; the
 // generated `body(v, r)` is the block's primitive sequence as straight-line code.
 struct NoEpi {
