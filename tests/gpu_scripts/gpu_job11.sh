@@ -5,7 +5,7 @@ timeout 1500 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&
 tail -3 gpurun_out/pytest_gpu.log
 {
 for spec in random:30:20:2 hea:30:5:4 qaoa:30:2:1 qft:30; do
-  python tests/_prof_ab.py $spec ""
-  QSV_JIT_SPLIT=0 python tests/_prof_ab.py $spec ""
+  python tests/gpu_scripts/prof_ab.py $spec ""
+  QSV_JIT_SPLIT=0 python tests/gpu_scripts/prof_ab.py $spec ""
 done
 } 2>&1 | grep -v Warning | tee gpurun_out/ab7.log

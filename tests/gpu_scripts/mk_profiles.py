@@ -1,9 +1,9 @@
 """Summarise a gpurun_out/ profiling run into profiles/ (tracked).
 
-Inputs (from tests/_gpu_job.sh): gpurun_out/bench.json, bench_ref.json, launches.csv
+Inputs (from tests/gpu_scripts/gpu_job.sh): gpurun_out/bench.json, bench_ref.json, launches.csv
 (ncu --metrics gpu__time_duration.sum launch list of the bench command) and
 prof_full.ncu-rep (ncu --set full of the heaviest pass).  Usage:
-    python tests/_mk_profiles.py r01 random:30:20:2
+    python tests/gpu_scripts/mk_profiles.py r01 random:30:20:2
 """
 import csv
 import io
