@@ -145,7 +145,7 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
     const int NT = threads_for_k(K);
     const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
     std::ostringstream o;
-    minb = K >= 12 ? 1 : (NT >= 256 ? 2 : 3);
+    minb = K >= 12 ? 1 : 3;
     for (int i = 0; i < s.nops; ++i) {
         const TileOp& op = ops[i];
         const std::string opref = "*reinterpret_cast<const qsv::TileOp*>(blob + " +
