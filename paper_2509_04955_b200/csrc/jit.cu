@@ -116,10 +116,12 @@ const Driver& driver() {
 
 // ------------------------------------------------------------------ codegen
 // Split register blocks (two threads per 16-member group, 256 threads for 11-qubit
-// tiles); QSV_JIT_SPLIT=0 keeps one thread per group.
+// tiles, 3 CTAs/SM at 80 registers): measured slower than one thread per group
+// (random-30 345 vs 310 ms, HEA-30 133 vs 120 ms; profiles/README.md), so opt-in
+// with QSV_JIT_SPLIT=1.
 bool split_blocks() {
     const char* e = std::getenv("QSV_JIT_SPLIT");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
 }
 int threads_for_k(int K) {
     if (K == 11 && split_blocks())

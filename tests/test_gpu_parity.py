@@ -58,6 +58,16 @@ def test_generated_circuits_vs_oracle(spec, opt):
     assert abs(norm - 1.0) <= NORM_TOL
 
 
+@pytest.mark.parametrize("spec", ["random:14:10:2", "hea:13:3:4", "uccsd:13:300:3"])
+def test_split_register_blocks_vs_oracle(spec, monkeypatch):  # opt-in QSV_JIT_SPLIT=1 kernels
+    monkeypatch.setenv("QSV_JIT_SPLIT", "1")
+    c = pkg.Circuit.generate(spec)
+    a = rand_state(c.n, 2)
+    got, norm = run_gpu(c, a, pkg.PlanOptions())
+    assert np.abs(got - O.run_local(c, a)).max() <= TOL
+    assert abs(norm - 1.0) <= NORM_TOL
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_random_mnemonic_circuits(seed):  # acceptance #1 on the GPU
     rng = np.random.default_rng(seed)

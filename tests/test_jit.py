@@ -32,6 +32,15 @@ CASES = [
 
 
 @pytest.mark.skipif(not _nvrtc_present(), reason="libnvrtc not in this image")
+def test_split_blocks_compile(monkeypatch):
+    monkeypatch.setenv("QSV_JIT_SPLIT", "1")  # opt-in variant: two threads per register group
+    c = pkg.Circuit.generate("random:16:8:2")
+    steps, ops, prims, pool = E.export_plan(c, pkg.PlanOptions(), c.n)
+    rc, nk = E.jit_check(steps, ops, prims, pool, c.n, c.n)
+    assert rc == 0, pkg.load_qsv().qsv_last_error()
+
+
+@pytest.mark.skipif(not _nvrtc_present(), reason="libnvrtc not in this image")
 @pytest.mark.parametrize("spec,kw", CASES)
 def test_jit_kernels_compile(spec, kw):
     # the cubin cache is keyed by the full generated source, so a cached hit is a
