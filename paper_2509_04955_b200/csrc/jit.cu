@@ -416,8 +416,8 @@ std::string kernel_source(const std::string& name, int K, int minb, const std::s
     o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb << ") " << name
       << "(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, uint32_t blob_bytes,\n"
       << "    const __grid_constant__ qsv::GeomArg geom, uint64_t rank_base, uint64_t ntiles) {\n"
-      << "  qsv::pass_pipeline<" << K << ", " << NT << ", " << tile_nbuf() << ", " << tile_pd()
-      << ">(psi, gblob, blob_bytes, geom, rank_base, ntiles,\n"
+      << "  qsv::pass_pipeline<" << K << ", " << NT << ", " << tile_nbuf() << ", " << tile_pd() << ", "
+      << (env_int("QSV_TMA_SPREAD", 1, 0, 1) ? "true" : "false") << ">(psi, gblob, blob_bytes, geom, rank_base, ntiles,\n"
       << "    [&](double2* tile, const unsigned char* blob, uint64_t full_base) {\n"
       << "  (void)full_base;\n"
       << body << "  });\n}\n";

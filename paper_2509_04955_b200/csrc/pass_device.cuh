@@ -661,7 +661,11 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const GeomArg& g) {
 // the buffer of tile t + PD - NBUF, whose store was committed NBUF - PD - 1
 // iterations before the current one, so warp 0 only waits for stores older than
 // that (NBUF = 2, PD = 1: the previous tile's store must have left SMEM).
-template <int K, int NT, int NBUF = kNumBuf, int PD = NBUF - 1, typename Ops>
+// SPREAD: every warp issues the TMA copies of its share of the runs (run j belongs to
+// warp j % NW) and arms the mbarrier for those bytes (one arrival per warp), instead of
+// warp 0 carrying all of it; each lane only ever waits for its own store groups, which
+// read exactly the SMEM runs it reloads.  Warps then reach the per-op barriers together.
+template <int K, int NT, int NBUF = kNumBuf, int PD = NBUF - 1, bool SPREAD = true, typename Ops>
 __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const unsigned char* __restrict__ gblob,
                                               uint32_t blob_bytes, const GeomArg& geom, uint64_t rank_base,
                                               uint64_t ntiles, Ops&& ops) {
@@ -695,28 +699,34 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         for (uint32_t i = threadIdx.x; i < blob_bytes / 16; i += NT)
             dst[i] = __ldg(src + i);
     }
+    constexpr int NW = SPREAD ? NT / 32 : 1;  // warps issuing TMA copies
     if (threadIdx.x == 0) {
         for (int b = 0; b < NBUF; ++b)
-            mbar_init(&mbar[b], 1);
+            mbar_init(&mbar[b], NW);
         fence_mbar_init();
     }
     __syncthreads();
 
     const uint64_t stride = gridDim.x;
-    // Warp 0 drives the TMA bulk engine: lane 0 arms the tile's mbarrier with the
-    // byte count, then the 32 lanes issue the 2^nhigh run copies between them.
+    // The issuing warps drive the TMA bulk engine: lane 0 of each arms the tile's
+    // mbarrier with its byte count, then its lanes issue that warp's run copies.
     const int lane = threadIdx.x & 31;
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    const bool issuer = warp < NW;
+    const int my_runs = nruns > warp ? (nruns - warp + NW - 1) / NW : 0;
     auto issue_load = [&](uint64_t t, int b) {
         const uint64_t base = tile_base(geom.tile0 + t, geom);
         double2* dst = bufs + b * TILE;
         if (lane == 0)
-            mbar_expect_tx(&mbar[b], static_cast<uint32_t>(sizeof(double2) * TILE));
+            mbar_expect_tx(&mbar[b], static_cast<uint32_t>(my_runs) * run_bytes);
         __syncwarp();
-        for (int j = lane; j < nruns; j += 32)
+        for (int k = lane; k < my_runs; k += 32) {
+            const int j = warp + NW * k;
             bulk_load(dst + (j << RL), psi + base + hi_off[j << m], run_bytes, &mbar[b]);
+        }
     };
 
-    if (threadIdx.x < 32) {
+    if (issuer) {
         for (int s = 0; s < PD; ++s) {
             const uint64_t t = blockIdx.x + s * stride;
             if (t < ntiles)
@@ -727,7 +737,7 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     int it = 0;
     for (uint64_t t = blockIdx.x; t < ntiles; t += stride, ++it) {
         const int b = it % NBUF;
-        if (threadIdx.x < 32) {
+        if (issuer) {
             const uint64_t tn = t + PD * stride;
             if (tn < ntiles) {
                 // Buffer (it + PD) % NBUF was last stored from in iteration
@@ -747,13 +757,15 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         // (async) proxy, then let thread 0 stream the tile back.
         fence_proxy_async();
         __syncthreads();
-        if (threadIdx.x < 32) {
-            for (int j = lane; j < nruns; j += 32)
+        if (issuer) {
+            for (int k = lane; k < my_runs; k += 32) {
+                const int j = warp + NW * k;
                 bulk_store(psi + base + hi_off[j << m], tile + (j << RL), run_bytes);
+            }
             bulk_commit();
         }
     }
-    if (threadIdx.x < 32)
+    if (issuer)
         bulk_wait_all();
 }
 
