@@ -1262,9 +1262,14 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
         int done = 0;
         while (done < nops) {
             int pick = -1;
+            // local ops that join the open pass first, then any local op
             for (int i : ready)
-                if (is_local(i) && (pick < 0 || i < pick))
+                if (is_local(i) && (pick < 0 || i < pick) && pk.fits(ops[i]))
                     pick = i;
+            if (pick < 0)
+                for (int i : ready)
+                    if (is_local(i) && (pick < 0 || i < pick))
+                        pick = i;
             if (pick < 0) {
                 pick = *std::min_element(ready.begin(), ready.end());
                 const std::vector<int> need = local_needs(ops[pick]);
