@@ -77,3 +77,16 @@ def test_qft_large_distributed_analytic(two):
     c = pkg.Circuit.generate("qft:28")
     got, rep = run_dist(c, 1, 20, 2)
     assert np.abs(got - 2.0 ** (-14)).max() <= 1e-10
+
+
+@pytest.mark.parametrize("mode", [{"QSV_SWAP_MODE": "nccl"}, {"QSV_OVERLAP": "1"},
+                                  {"QSV_OVERLAP": "1", "QSV_SWAP_MODE": "nccl"}])
+@pytest.mark.parametrize("spec", ["random:20:10:2", "qaoa:18:2:1", "uccsd:18:600:3"])
+def test_two_gpu_swap_paths(two, spec, mode, monkeypatch):
+    """The NCCL chunked swap and the (opt-in) region-overlap schedules give the same
+    amplitudes as the oracle (the default P2P swap is covered above)."""
+    for k, v in mode.items():
+        monkeypatch.setenv(k, v)
+    c = pkg.Circuit.generate(spec)
+    got, rep = run_dist(c, 1, 12, 2)
+    assert np.abs(got - O.run_local(c)).max() <= 1e-10
