@@ -262,6 +262,37 @@ class Circuit:
         _check(load_qsim().qsim_circuit_export(self._h, recs, _dptr(pool.view(np.float64))), "export")
         return n, recs, nr, pool
 
+    def inverse(self) -> "Circuit":
+        """C^dagger: the gates in reverse order with adjoint matrices (barriers dropped);
+        C followed by C^dagger maps every state to itself (mirror-circuit checks)."""
+        n, recs, nr, pool = self.export()
+        out = Circuit.empty(n)
+        for i in reversed(range(nr)):
+            r = recs[i]
+            if r.arity == 0:
+                continue
+            d = 1 << r.arity
+            m = pool[r.mat_off:r.mat_off + d * d].reshape(d, d)
+            out.add_unitary(m.conj().T, list(r.targets[:r.arity]), list(r.controls[:r.nctrl]), "INV")
+        return out
+
+    def concat(self, other: "Circuit") -> "Circuit":
+        """This circuit followed by `other` (same qubit count)."""
+        n, recs, nr, pool = self.export()
+        n2, recs2, nr2, pool2 = other.export()
+        if n != n2:
+            raise ValueError("concat: qubit counts differ")
+        out = Circuit.empty(n)
+        for rr, k, pl in ((recs, nr, pool), (recs2, nr2, pool2)):
+            for i in range(k):
+                r = rr[i]
+                if r.arity == 0:
+                    continue
+                d = 1 << r.arity
+                out.add_unitary(pl[r.mat_off:r.mat_off + d * d].reshape(d, d), list(r.targets[:r.arity]),
+                                list(r.controls[:r.nctrl]), "G")
+        return out
+
     def slice(self, begin: int, end: int) -> "Circuit":
         h = C.c_void_p()
         _check(load_qsim().qsim_circuit_slice(self._h, C.c_int64(begin), C.c_int64(end), C.byref(h)), "slice")

@@ -212,3 +212,30 @@ def test_random30_fusion_on_vs_off_and_norm():  # configs[1] at full size: DAGC 
     assert e2.max_abs_diff(ref, 0) <= TOL
     assert e2.max_abs_diff(tail, (1 << 30) - (1 << 20)) <= TOL
     e2.close()
+
+
+def _mirror_check(spec, opts=None):
+    """C then C^dagger on |0...0> must return |0...0> (SURVEY §8c mirror circuits): checked
+    on the device at sizes the CPU oracle cannot hold."""
+    c = pkg.Circuit.generate(spec)
+    m = c.concat(c.inverse())
+    e = pkg.Engine(m, opts or pkg.PlanOptions())
+    e.set_basis(0)
+    e.run()
+    e.sync()
+    a0 = e.download(0, 1)[0]
+    norm = e.norm_sq()
+    e.close()
+    # |<0|psi>|^2 = 1 - sum_{x>0} |psi_x|^2: the rest of the state is bounded by the norm
+    return abs(a0 - 1.0), abs(norm - 1.0)
+
+
+@pytest.mark.parametrize("spec", ["random:30:20:2", "hea:30:5:4", "uccsd:26:3000:3"])
+def test_mirror_full_size(spec):  # configs[1..3] shapes at full size
+    err0, nerr = _mirror_check(spec)
+    assert err0 <= 1e-10 and nerr <= 1e-12
+
+
+def test_mirror_hea33_128GiB():  # configs[3]: 33 qubits, 128 GiB on one B200
+    err0, nerr = _mirror_check("hea:33:5:4")
+    assert err0 <= 1e-10 and nerr <= 1e-12
