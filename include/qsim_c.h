@@ -50,6 +50,7 @@ typedef struct qsim_plan_opts {
     double max_sweeps;        /* SMEM sweeps of the tile per pass                */
     int32_t list_schedule;    /* single rank: also try a DAG list schedule       */
     int32_t jit_max_kernels;  /* distinct specialised pass kernels compiled at most */
+    int32_t logical_swaps;    /* also plan SWAP gates (CX triples) as relabellings  */
 } qsim_plan_opts;
 
 typedef struct qsim_plan_stats {

@@ -60,6 +60,7 @@ class qsim_plan_opts(C.Structure):
         ("max_sweeps", C.c_double),
         ("list_schedule", C.c_int32),
         ("jit_max_kernels", C.c_int32),
+        ("logical_swaps", C.c_int32),
     ]
 
 
@@ -159,6 +160,7 @@ class PlanOptions:
     max_sweeps: float = 8.0
     list_schedule: bool = True
     jit_max_kernels: int = 8192
+    logical_swaps: int = 1  # 0 off, 1 when cheaper, 2 always
 
     @classmethod
     def default(cls) -> "PlanOptions":
@@ -166,14 +168,15 @@ class PlanOptions:
         load_qsim().qsim_default_opts(C.byref(o))
         return cls(o.tile_k, o.min_low, o.fuse_k, bool(o.fusion), bool(o.multi_op_passes),
                    o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k, bool(o.jit),
-                   int(o.relabel), o.max_sweeps, bool(o.list_schedule), o.jit_max_kernels)
+                   int(o.relabel), o.max_sweeps, bool(o.list_schedule), o.jit_max_kernels,
+                   int(o.logical_swaps))
 
     def to_c(self) -> qsim_plan_opts:
         return qsim_plan_opts(self.tile_k, self.min_low, self.fuse_k, int(self.fusion),
                               int(self.multi_op_passes), self.chunk_log2, self.nbuf,
                               int(self.register_blocks), float(self.pass_budget), int(self.rblock_k),
                               int(self.jit), int(self.relabel), float(self.max_sweeps),
-                              int(self.list_schedule), int(self.jit_max_kernels))
+                              int(self.list_schedule), int(self.jit_max_kernels), int(self.logical_swaps))
 
 
 class Circuit:

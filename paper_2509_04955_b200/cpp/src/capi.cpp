@@ -69,6 +69,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.max_sweeps = o->max_sweeps;
     p.list_schedule = o->list_schedule != 0;
     p.jit_max_kernels = o->jit_max_kernels;
+    p.logical_swaps = o->logical_swaps;
     return p;
 }
 
@@ -126,6 +127,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->max_sweeps = p.max_sweeps;
     out->list_schedule = p.list_schedule;
     out->jit_max_kernels = p.jit_max_kernels;
+    out->logical_swaps = p.logical_swaps;
 }
 
 int qsim_circuit_generate(const char* spec, qsim_circuit** out) {

@@ -228,7 +228,7 @@ Op make_phaseprod(const Op& A, const Op& B, const std::vector<int>& C, const Fac
 // Merge B (later) into A (earlier); false when no legal/within-limit merge exists.
 bool merge_ops(const Op& A, const Op& B, int fuse_k, int min_low, int max_high, Op& out) {
     if (A.kind == OpKind::Fence || B.kind == OpKind::Fence || A.kind == OpKind::RBlock ||
-        B.kind == OpKind::RBlock)
+        B.kind == OpKind::RBlock || A.kind == OpKind::Swap || B.kind == OpKind::Swap)
         return false;
     if (diag_like(A) && diag_like(B)) {
         // (1) separable phase product under the common controls
@@ -296,7 +296,7 @@ bool merge_ops(const Op& A, const Op& B, int fuse_k, int min_low, int max_high, 
 }
 
 bool is_identity(const Op& o) {
-    if (o.kind == OpKind::XPerm || o.kind == OpKind::Fence || o.kind == OpKind::RBlock)
+    if (o.kind == OpKind::XPerm || o.kind == OpKind::Fence || o.kind == OpKind::RBlock || o.kind == OpKind::Swap)
         return false;
     if (o.kind == OpKind::PhaseProd) {
         if (o.data[0] != Amp{1.0, 0.0})
@@ -412,7 +412,8 @@ double op_cost(const Op& o) {
             c += prim_cost(p);
         return c;
     }
-    case OpKind::Fence: return 0.0;
+    case OpKind::Fence:
+    case OpKind::Swap: return 0.0;
     }
     return 0.0;
 }
@@ -1017,7 +1018,8 @@ struct Packer {
             break;
         }
         case OpKind::Fence:
-            throw std::logic_error("to_desc: fence");
+        case OpKind::Swap:
+            throw std::logic_error("to_desc: fence/swap have no device op");
         }
         return d;
     }
@@ -1044,7 +1046,7 @@ struct Packer {
 
     // Would `o` join the open pass without closing it?
     bool fits(const Op& o) const {
-        if (cur_ops.empty())
+        if (cur_ops.empty() || o.kind == OpKind::Swap)
             return true;
         std::vector<int> need = targets;
         for (int p : tile_needs(o))
@@ -1057,6 +1059,11 @@ struct Packer {
     }
 
     void add(const Op& o) {
+        if (o.kind == OpKind::Swap) {
+            // SWAP as a relabelling: the two logical qubits trade physical slots
+            std::swap(pos[o.qubits[0]], pos[o.qubits[1]]);
+            return;
+        }
         std::vector<int> need = targets;
         for (int p : tile_needs(o))
             if (!contains(need, p))
@@ -1121,6 +1128,56 @@ std::vector<int> local_needs(const Op& o) {
 }
 
 } // namespace
+
+// CX(a,b) CX(b,a) CX(a,b) with nothing else on a or b in between is a SWAP of a and b:
+// replaced by one Swap op (planned as a free relabelling).  Returns the number found.
+int find_logical_swaps(std::vector<Op>& ops) {
+    auto cx = [](const Op& o, int& c, int& t) {
+        if (o.kind != OpKind::XPerm || o.controls.size() != 1 || o.qubits.size() != 1)
+            return false;
+        c = o.controls[0];
+        t = o.qubits[0];
+        return true;
+    };
+    int nq = 0;
+    for (const Op& o : ops)
+        for (int q : footprint(o))
+            nq = std::max(nq, q + 1);
+    std::vector<std::vector<int>> wire(static_cast<std::size_t>(nq));  // live op indices per qubit
+    std::vector<char> dead(ops.size(), 0);
+    int found = 0;
+    for (int i = 0; i < static_cast<int>(ops.size()); ++i) {
+        int c, t, c1, t1, c2, t2;
+        if (cx(ops[i], c, t) && wire[c].size() >= 2 && wire[t].size() >= 2) {
+            const int j = wire[c].back(), k = wire[c][wire[c].size() - 2];
+            if (wire[t].back() == j && wire[t][wire[t].size() - 2] == k && cx(ops[j], c1, t1) && c1 == t &&
+                t1 == c && cx(ops[k], c2, t2) && c2 == c && t2 == t) {
+                Op sw;
+                sw.kind = OpKind::Swap;
+                sw.qubits = {std::min(c, t), std::max(c, t)};
+                sw.first_gate = ops[k].first_gate;
+                sw.last_gate = ops[i].last_gate;
+                sw.ngates = 3;
+                ops[k] = sw;
+                dead[j] = 1;
+                dead[i] = 1;
+                wire[c].pop_back();
+                wire[t].pop_back();
+                ++found;
+                continue;
+            }
+        }
+        for (int q : footprint(ops[i]))
+            wire[q].push_back(i);
+    }
+    std::vector<Op> out;
+    out.reserve(ops.size());
+    for (std::size_t i = 0; i < ops.size(); ++i)
+        if (!dead[i])
+            out.push_back(std::move(ops[i]));
+    ops = std::move(out);
+    return found;
+}
 
 // Relative time of a plan in units of one HBM round trip, from the B200
 // measurements in profiles/ (r01): a relabel costs an extra SMEM sweep (~17 % of
@@ -1385,22 +1442,13 @@ static void finish_plan(const Circuit& c, const PlanOptions& opt, Packer& pk, Pl
     }
 }
 
-Plan make_plan(const Circuit& c, const PlanOptions& opt) {
-    c.validate();
-    if (opt.fuse_k < 1 || opt.fuse_k > QSV_MAX_DENSE_K)
-        throw std::invalid_argument("make_plan: fuse_k must be in [1, 5]");
-    if (opt.tile_k < 1 || opt.tile_k > QSV_MAX_TILE_K)
-        throw std::invalid_argument("make_plan: tile_k must be in [1, 12] (12 needs the specialised kernels)");
-    if (opt.rblock_k != 3 && opt.rblock_k != 4)
-        throw std::invalid_argument("make_plan: rblock_k must be 3 or 4");
-    Plan plan;
-    plan.n = c.n;
-    plan.n_local = opt.n_local < 0 ? c.n : opt.n_local;
-    if (plan.n_local < 1 || plan.n_local > c.n)
-        throw std::invalid_argument("make_plan: n_local must be in [1, n]");
-    plan.stats.gates_in = c.gate_count();
-    std::vector<Op> ops = lower(c);
+// The DAGC stages: lower -> (logical swaps) -> parity peephole -> fuse -> register blocks.
+// Returns false when `swaps` is requested but the circuit has no SWAP triple.
+static bool build_ops(const Circuit& c, const PlanOptions& opt, bool swaps, Plan& plan, std::vector<Op>& ops) {
+    ops = lower(c);
     plan.stats.ops_lowered = ops.size();
+    if (swaps && find_logical_swaps(ops) == 0)
+        return false;
     if (opt.fusion) {
         ops = reduce_parity(ops);
         PlanOptions fo = opt;
@@ -1420,16 +1468,19 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
         ops = form_blocks(ops, std::min(opt.min_low, K), std::min(QSV_MAX_HIGH, K - std::min(opt.min_low, K)),
                           opt.rblock_k);
     plan.stats.ops_final = ops.size();
+    plan.stats.cost_units = 0;
+    plan.stats.max_dense_k = 0;
     for (const Op& o : ops) {
         plan.stats.cost_units += op_cost(o);
         if (o.kind == OpKind::Dense)
             plan.stats.max_dense_k = std::max(plan.stats.max_dense_k, static_cast<int>(o.qubits.size()));
     }
+    return true;
+}
 
-    // Tile relabelling is a per-circuit win or loss (lookahead saves passes, the final
-    // restore costs some): plan both ways and keep the one with fewer HBM passes.
-    if (opt.relabel < 0 || opt.relabel > 2)
-        throw std::invalid_argument("make_plan: relabel must be 0, 1 or 2");
+// Packing candidates for one op list: {program order, list schedule} x {plain,
+// relabelled}; the one the time model rates fastest wins.
+static Plan choose_pack(const Circuit& c, std::vector<Op> ops, const PlanOptions& opt, const Plan& plan) {
     PlanOptions o_plain = opt;
     o_plain.relabel = 0;
     const bool single = plan.n_local == c.n;
@@ -1463,6 +1514,40 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     return best;
 }
 
+Plan make_plan(const Circuit& c, const PlanOptions& opt) {
+    c.validate();
+    if (opt.fuse_k < 1 || opt.fuse_k > QSV_MAX_DENSE_K)
+        throw std::invalid_argument("make_plan: fuse_k must be in [1, 5]");
+    if (opt.tile_k < 1 || opt.tile_k > QSV_MAX_TILE_K)
+        throw std::invalid_argument("make_plan: tile_k must be in [1, 12] (12 needs the specialised kernels)");
+    if (opt.rblock_k != 3 && opt.rblock_k != 4)
+        throw std::invalid_argument("make_plan: rblock_k must be 3 or 4");
+    if (opt.relabel < 0 || opt.relabel > 2)
+        throw std::invalid_argument("make_plan: relabel must be 0, 1 or 2");
+    Plan plan;
+    plan.n = c.n;
+    plan.n_local = opt.n_local < 0 ? c.n : opt.n_local;
+    if (plan.n_local < 1 || plan.n_local > c.n)
+        throw std::invalid_argument("make_plan: n_local must be in [1, n]");
+    plan.stats.gates_in = c.gate_count();
+    std::vector<Op> ops;
+    Plan base = plan;
+    build_ops(c, opt, false, base, ops);
+    Plan best = choose_pack(c, std::move(ops), opt, base);
+    if (opt.logical_swaps < 0 || opt.logical_swaps > 2)
+        throw std::invalid_argument("make_plan: logical_swaps must be 0, 1 or 2");
+    if (opt.logical_swaps && opt.fusion) {
+        // SWAP gates as relabellings: free when the final layout restore is cheap
+        Plan sb = plan;
+        if (build_ops(c, opt, true, sb, ops)) {
+            Plan alt = choose_pack(c, std::move(ops), opt, sb);
+            if (opt.logical_swaps == 2 || plan_time_model(alt) < plan_time_model(best))
+                best = std::move(alt);
+        }
+    }
+    return best;
+}
+
 Circuit ops_to_circuit(int n, const std::vector<Op>& ops) {
     Circuit c(n, "fused");
     auto add_matrix = [&](std::vector<int> t, std::vector<int> ctl, std::vector<Amp> m) {
@@ -1482,6 +1567,11 @@ Circuit ops_to_circuit(int n, const std::vector<Op>& ops) {
     for (const Op& o : ops) {
         switch (o.kind) {
         case OpKind::Fence: break;
+        case OpKind::Swap:
+            add_matrix({o.qubits[1]}, {o.qubits[0]}, {0.0, 1.0, 1.0, 0.0});
+            add_matrix({o.qubits[0]}, {o.qubits[1]}, {0.0, 1.0, 1.0, 0.0});
+            add_matrix({o.qubits[1]}, {o.qubits[0]}, {0.0, 1.0, 1.0, 0.0});
+            break;
         case OpKind::Dense: add_matrix(o.qubits, o.controls, o.data); break;
         case OpKind::XPerm: add_matrix(o.qubits, o.controls, {0.0, 1.0, 1.0, 0.0}); break;
         case OpKind::Diag:

@@ -85,3 +85,29 @@ def test_two_rank_plan_matches_oracle(spec, kw):
     err, nswaps = q.get(timeout=5)
     assert err < 1e-10
     assert nswaps >= 1  # the global qubit was touched, so the plan exchanged data
+
+
+def test_two_rank_logical_swaps(tmp_path):
+    """A circuit full of SWAP gates, planned with SWAPs as relabellings (logical_swaps=2),
+    across two ranks: global qubits move through relabelling as well as qubit swaps."""
+    rng = np.random.default_rng(9)
+    lines = ["OPENQASM 2.0;", "qreg q[11];"]
+    for _ in range(50):
+        a, b = (int(x) for x in rng.choice(11, 2, replace=False))
+        k = rng.integers(0, 3)
+        lines.append(f"swap q[{a}],q[{b}];" if k == 0 else
+                     (f"ry({rng.uniform(0, 6.28)}) q[{a}];" if k == 1 else f"cx q[{a}],q[{b}];"))
+    path = tmp_path / "swaps.qasm"
+    path.write_text("\n".join(lines))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, f"qasm:{path}", {"logical_swaps": 2}, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    err, nswaps = q.get(timeout=5)
+    assert err < 1e-10

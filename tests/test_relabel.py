@@ -71,3 +71,34 @@ def test_list_schedule_never_worse():
         on = c.plan(pkg.PlanOptions(tile_k=8))["passes"]
         off = c.plan(pkg.PlanOptions(tile_k=8, list_schedule=False, relabel=0))["passes"]
         assert on <= off
+
+
+def _swap_heavy(n, seed):
+    """Random circuit with explicit SWAP gates (QASM `swap` -> three CX)."""
+    rng = np.random.default_rng(seed)
+    lines = ["OPENQASM 2.0;", f"qreg q[{n}];"]
+    for _ in range(60):
+        a, b = (int(x) for x in rng.choice(n, 2, replace=False))
+        k = rng.integers(0, 3)
+        if k == 0:
+            lines.append(f"swap q[{a}],q[{b}];")
+        elif k == 1:
+            lines.append(f"rx({rng.uniform(0, 6.28)}) q[{a}];")
+        else:
+            lines.append(f"cx q[{a}],q[{b}];")
+    return pkg.Circuit.from_qasm("\n".join(lines))
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("kw", [dict(logical_swaps=2), dict(tile_k=7, min_low=3, logical_swaps=2),
+                                dict(relabel=0, list_schedule=False, logical_swaps=2), dict(tile_k=7, min_low=3)])
+def test_logical_swaps_match_oracle(seed, kw):
+    """SWAP gates planned as relabellings (logical_swaps) give the oracle's amplitudes."""
+    c = _swap_heavy(11, seed)
+    steps, ops, prims, pool = E.export_plan(c, pkg.PlanOptions(**kw), c.n)
+    a = rand_state(c.n, seed)
+    psi = E.run_program(a.copy(), steps, ops, prims, pool, 0, c.n, None)
+    assert np.abs(psi - O.run_local(c, a)).max() < 1e-10
+    # the fused op list (with swaps re-expanded) is equivalent too
+    f = c.fused(pkg.PlanOptions(**kw))
+    assert np.abs(O.run_local(f, a) - O.run_local(c, a)).max() < 1e-10
