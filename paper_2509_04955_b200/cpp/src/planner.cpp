@@ -1464,9 +1464,14 @@ static bool build_ops(const Circuit& c, const PlanOptions& opt, bool swaps, Plan
     }
     plan.stats.ops_fused = ops.size();
     const int K = std::min(opt.tile_k, plan.n_local);
-    if (opt.fusion && opt.register_blocks && K >= std::max(opt.min_low, 5) && opt.multi_op_passes)
-        ops = form_blocks(ops, std::min(opt.min_low, K), std::min(QSV_MAX_HIGH, K - std::min(opt.min_low, K)),
-                          opt.rblock_k);
+    if (opt.fusion && opt.register_blocks && K >= std::max(opt.min_low, 5) && opt.multi_op_passes) {
+        const int lo = std::min(opt.min_low, K);
+        const int max_high = std::min(QSV_MAX_HIGH, K - lo);
+        // with SWAPs relabelled any logical qubit may sit above the low run: blocks must
+        // then fit the high slots on their own
+        ops = swaps ? form_blocks(ops, 0, max_high, std::min(opt.rblock_k, std::max(max_high, 3)))
+                    : form_blocks(ops, lo, max_high, opt.rblock_k);
+    }
     plan.stats.ops_final = ops.size();
     plan.stats.cost_units = 0;
     plan.stats.max_dense_k = 0;
@@ -1539,10 +1544,15 @@ Plan make_plan(const Circuit& c, const PlanOptions& opt) {
     if (opt.logical_swaps && opt.fusion) {
         // SWAP gates as relabellings: free when the final layout restore is cheap
         Plan sb = plan;
-        if (build_ops(c, opt, true, sb, ops)) {
-            Plan alt = choose_pack(c, std::move(ops), opt, sb);
-            if (opt.logical_swaps == 2 || plan_time_model(alt) < plan_time_model(best))
-                best = std::move(alt);
+        try {
+            if (build_ops(c, opt, true, sb, ops)) {
+                Plan alt = choose_pack(c, std::move(ops), opt, sb);
+                if (opt.logical_swaps == 2 || plan_time_model(alt) < plan_time_model(best))
+                    best = std::move(alt);
+            }
+        } catch (const std::logic_error&) {
+            if (opt.logical_swaps == 2)
+                throw;  // forced: report why the relabelled plan is infeasible
         }
     }
     return best;
