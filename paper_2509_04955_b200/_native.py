@@ -160,7 +160,7 @@ class PlanOptions:
     max_sweeps: float = 8.0
     list_schedule: bool = True
     jit_max_kernels: int = 8192
-    logical_swaps: int = 1  # 0 off, 1 when cheaper, 2 always
+    logical_swaps: int = 0  # 0 off, 1 when the time model prefers it, 2 always
 
     @classmethod
     def default(cls) -> "PlanOptions":

@@ -72,7 +72,7 @@ struct PlanOptions {
     int nbuf = 2;             // BBOP buffers B (default 2)
     bool jit = true;          // NVRTC-specialised pass kernels (falls back to the interpreter kernel)
     int jit_max_kernels = 8192; // distinct pass structures compiled at most (the rest interpreted)
-    int logical_swaps = 1;    // SWAP gates (CX triples) as free relabellings: 0 off, 1 when the
+    int logical_swaps = 0;    // SWAP gates (CX triples) as free relabellings: 0 off, 1 when the
                               // time model prefers it, 2 always (tests)
     int relabel = 1;          // tile-qubit relabelling at pass ends: 0 off, 1 auto (kept when it
                               // saves passes), 2 always (tests)
