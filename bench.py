@@ -467,7 +467,7 @@ def main():
         "circuit_time_s": ms_step / 1e3,
         "hbm_gbs_avg": (sum(pass_bytes) / 1e9) / (sum(pass_ms) / 1e3) if pass_ms else None,
         "roofline": {
-            "bound": "hbm", "kernel": "qsv::pass_kernel (fused multi-block pass)",
+            "bound": "hbm", "kernel": "qsv_jit_* (NVRTC-specialised fused multi-op pass kernels; qsv::pass_kernel is the interpreter fallback)",
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
             "peak_source": hbm_src,
