@@ -183,8 +183,20 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
         case QSV_OP_RBLOCK: {
             // Diagonal ops right after a whole-tile register block ride along as a
             // per-amplitude epilogue: no extra SMEM sweep or barrier for them.
-            std::ostringstream pre, epi;
+            std::ostringstream pre, epi, epib;
             int last = i;
+            const int KBm = op.k;
+            uint32_t mm[4] = {0, 0, 0, 0};
+            for (int jj = 0; jj < KBm; ++jj)
+                mm[jj] = 1u << op.tpos[jj];
+            auto offj = [&](int j) {
+                uint32_t o2 = 0;
+                for (int bb = 0; bb < KBm; ++bb)
+                    if ((j >> bb) & 1)
+                        o2 ^= mm[bb];
+                return o2;
+            };
+            const int NVm = 1 << KBm;
             if (op.xctrl == 0 && op.tctrl == 0 && !std::getenv("QSV_JIT_NO_EPI")) {
                 for (int j = i + 1; j < s.nops; ++j) {
                     const TileOp& d = ops[j];
@@ -233,6 +245,32 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
                         stmt = "a = qsv::cmul((__popc(idx & " + u32(d.tmask) + ") & 1) ? p" + J + "b : p" + J + "a, a);";
                     }
                     epi << "    " << (guard.empty() ? "" : "if (" + guard + ") ") << stmt << "\n";
+                    // block form: per member, with the PHASEPROD table loads shared
+                    std::map<uint32_t, std::string> lo_var, hi_var;
+                    if (d.kind == QSV_OP_PHASEPROD) {
+                        const std::string tab = "reinterpret_cast<const double2*>(blob + " + std::to_string(d.mat_byte) + ")";
+                        for (int jm = 0; jm < NVm; ++jm) {
+                            const uint32_t lo = offj(jm) & 31u, hi = offj(jm) >> 5;
+                            if (!lo_var.count(lo)) {
+                                lo_var[lo] = "pa" + J + "_" + std::to_string(lo);
+                                epib << "    const double2 " << lo_var[lo] << " = " << tab << "[1u + ((base ^ " << u32(lo)
+                                     << ") & 31u)];\n";
+                            }
+                            if (!hi_var.count(hi)) {
+                                hi_var[hi] = "pb" + J + "_" + std::to_string(hi);
+                                epib << "    const double2 " << hi_var[hi] << " = " << tab << "[33u + ((base >> 5) ^ " << u32(hi)
+                                     << ")];\n";
+                            }
+                        }
+                    }
+                    for (int jm = 0; jm < NVm; ++jm) {
+                        std::string st = stmt, g = guard;
+                        if (d.kind == QSV_OP_PHASEPROD)
+                            st = "a = qsv::cmul(qsv::cmul(c" + J + ", qsv::cmul(" + lo_var[offj(jm) & 31u] + ", " +
+                                 hi_var[offj(jm) >> 5] + ")), a);";
+                        epib << "    { double2& a = v[" << jm << "]; const uint32_t idx = base ^ " << u32(offj(jm))
+                             << "; (void)idx; " << (g.empty() ? "" : "if (" + g + ") ") << st << " }\n";
+                    }
                     last = j;
                 }
             }
@@ -381,7 +419,7 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
                 }
             }
             if (last > i) {
-                o << "  }, [&](double2& a, uint32_t idx) {\n    (void)idx;\n" << epi.str() << "  });\n";
+                o << "  }, qsv::NoEpi{}, [&](double2 (&v)[" << NV << "], uint32_t base) {\n" << epib.str() << "  });\n";
                 i = last;  // the fused diagonal ops are done
             } else {
                 o << "  });\n";

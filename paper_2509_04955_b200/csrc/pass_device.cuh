@@ -910,11 +910,19 @@ struct NoEpi {
     __device__ __forceinline__ void operator()(double2&, uint32_t) const {}
 };
 
+// Block epilogue: `epib(v, base)` sees every register of the group at once (the JIT
+// emits straight-line code with the diagonal-table loads that several members share
+// issued once); runs before any store.
+struct NoEpiB {
+    template <int NV>
+    __device__ __forceinline__ void operator()(double2 (&)[NV], uint32_t) const {}
+};
+
 // `epi(v, idx)` (JIT diagonal epilogue) runs on every amplitude before it is
 // written back; only used when the block covers the whole tile (TCTRL == 0).
 template <int K, int NT, int KB, uint32_t F, uint32_t TCTRL, uint32_t M0, uint32_t M1, uint32_t M2, uint32_t M3,
-          uint32_t ROT, typename Body, typename Epi = NoEpi>
-__device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi = Epi{}) {
+          uint32_t ROT, typename Body, typename Epi = NoEpi, typename EpiB = NoEpiB>
+__device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi = Epi{}, EpiB&& epib = EpiB{}) {
     constexpr int NV = 1 << KB;
     constexpr uint32_t groups = 1u << (K - cpopc(F));
     constexpr uint32_t dstep = cdeposit(NT, F);
@@ -932,6 +940,7 @@ __device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi
         for (int j = 0; j < NV; ++j)
             v[j] = tile[base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))];
         body(v, r);
+        epib(v, base);
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const uint32_t idx = base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u));
