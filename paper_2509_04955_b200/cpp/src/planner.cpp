@@ -1317,6 +1317,8 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
             return true;
         };
         int done = 0;
+        std::vector<char> placed(static_cast<std::size_t>(nops), 0);
+        const bool remaining_only = std::getenv("QSV_VICTIM_REMAINING") != nullptr;
         while (done < nops) {
             int pick = -1;
             // local ops that join the open pass first, then any local op
@@ -1334,7 +1336,22 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
                     if (pk.pos[q] < plan.n_local)
                         continue;
                     // victims: local, not needed by this op, preferably outside the low
-                    // run (contiguous swap chunks) and outside the open pass's tile
+                    // run (contiguous swap chunks) and outside the open pass's tile;
+                    // Belady: the qubit whose next local use is farthest, then the one
+                    // with the fewest remaining uses, then the highest slot
+                    std::vector<long long> next_need(static_cast<std::size_t>(c.n), 1LL << 40);
+                    if (!remaining_only) {
+                        int found = 0;
+                        for (int i = 0; i < nops && found < c.n; ++i) {
+                            if (placed[i])
+                                continue;
+                            for (int x : local_needs(ops[i]))
+                                if (next_need[x] == (1LL << 40)) {
+                                    next_need[x] = i;
+                                    ++found;
+                                }
+                        }
+                    }
                     int best = -1;
                     for (int relax = 0; relax < 2 && best < 0; ++relax) {
                         long long best_score = std::numeric_limits<long long>::max();
@@ -1344,7 +1361,8 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
                                 continue;
                             if (relax == 0 && (p < pk.Lmin || contains(pk.targets, p)))
                                 continue;
-                            const long long score = static_cast<long long>(remaining[l]) * 64 - p;
+                            const long long score = -next_need[l] * (1LL << 20) +
+                                                    static_cast<long long>(remaining[l]) * 64 - p;
                             if (score < best_score) {
                                 best_score = score;
                                 best = l;
@@ -1361,6 +1379,7 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
                 }
             }
             ready.erase(std::find(ready.begin(), ready.end(), pick));
+            placed[pick] = 1;
             if (sched)
                 sched->order.push_back(pick);
             pk.add(ops[pick]);
