@@ -115,6 +115,8 @@ const Driver& driver() {
 }
 
 // ------------------------------------------------------------------ codegen
+int env_int(const char* name, int dflt, int lo, int hi);
+
 // Split register blocks (two threads per 16-member group, 256 threads for 11-qubit
 // tiles, 3 CTAs/SM at 80 registers): measured slower than one thread per group
 // (random-30 345 vs 310 ms, HEA-30 133 vs 120 ms; profiles/README.md), so opt-in
@@ -373,9 +375,25 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
                 }
                 break;
             }
+            // fold the pass relabel into this block's stores when it is the last op before it
+            bool fold = false;
+            std::string pmap;
+            if (last + 1 == s.nops - 1 && ops[last + 1].kind == QSV_OP_RELABEL && op.xctrl == 0 && op.tctrl == 0 &&
+                (1 << (K - __builtin_popcount(op.fmask))) == NT && env_int("QSV_JIT_FOLD_RELABEL", 1, 0, 1)) {
+                const TileOp& rl = ops[last + 1];
+                std::ostringstream pm;
+                pm << "[](uint32_t x) { return 0u";
+                for (int b = 0; b < K; ++b) {
+                    const int dst = b < 8 ? rl.tpos[b] : rl.xbit[b - 8];
+                    pm << " | (((x >> " << b << ") & 1u) << " << dst << ")";
+                }
+                pm << "; }";
+                pmap = pm.str();
+                fold = true;
+            }
             o << "  qsv::jit_rblock<" << K << ", " << NT << ", " << KB << ", " << u32(op.fmask) << ", "
               << u32(op.tctrl) << ", " << u32(m[0]) << ", " << u32(m[1]) << ", " << u32(m[2]) << ", " << u32(m[3])
-              << ", " << u32(op.rot_tab) << ">(tile, [&](double2 (&v)[" << NV << "], uint32_t r) {\n";
+              << ", " << u32(op.rot_tab) << (fold ? ", true" : "") << ">(tile, [&](double2 (&v)[" << NV << "], uint32_t r) {\n";
             if (last > i) {
                 // hoisted constants must precede the call: re-emit the call after them
                 std::string call = o.str();
@@ -418,7 +436,15 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
                     break;
                 }
             }
-            if (last > i) {
+            if (fold) {
+                o << "  }, qsv::NoEpi{}, ";
+                if (last > i)
+                    o << "[&](double2 (&v)[" << NV << "], uint32_t base) {\n" << epib.str() << "  }";
+                else
+                    o << "qsv::NoEpiB{}";
+                o << ", " << pmap << ");\n";
+                i = last + 1;  // the fused diagonal ops and the relabel are done
+            } else if (last > i) {
                 o << "  }, qsv::NoEpi{}, [&](double2 (&v)[" << NV << "], uint32_t base) {\n" << epib.str() << "  });\n";
                 i = last;  // the fused diagonal ops are done
             } else {

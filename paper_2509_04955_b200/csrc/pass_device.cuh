@@ -920,9 +920,18 @@ struct NoEpiB {
 
 // `epi(v, idx)` (JIT diagonal epilogue) runs on every amplitude before it is
 // written back; only used when the block covers the whole tile (TCTRL == 0).
+struct IdMap {
+    __device__ __forceinline__ uint32_t operator()(uint32_t x) const { return x; }
+};
+
+// PERM: the pass relabel folded into this (last, single-step, whole-tile) block: after
+// every thread has computed its group, members are stored through the XOR-linear tile-bit
+// permutation `map` instead of a separate relabel sweep.
 template <int K, int NT, int KB, uint32_t F, uint32_t TCTRL, uint32_t M0, uint32_t M1, uint32_t M2, uint32_t M3,
-          uint32_t ROT, typename Body, typename Epi = NoEpi, typename EpiB = NoEpiB>
-__device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi = Epi{}, EpiB&& epib = EpiB{}) {
+          uint32_t ROT, bool PERM = false, typename Body, typename Epi = NoEpi, typename EpiB = NoEpiB,
+          typename Map = IdMap>
+__device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi = Epi{}, EpiB&& epib = EpiB{},
+                                           Map&& map = Map{}) {
     constexpr int NV = 1 << KB;
     constexpr uint32_t groups = 1u << (K - cpopc(F));
     constexpr uint32_t dstep = cdeposit(NT, F);
@@ -941,11 +950,23 @@ __device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi
             v[j] = tile[base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))];
         body(v, r);
         epib(v, base);
+        if constexpr (PERM) {
+            static_assert(groups == static_cast<uint32_t>(NT), "folded relabel needs one group per thread");
+            __syncthreads();  // every member has been read before any permuted store
+            const uint32_t mb = map(base);
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const uint32_t idx = base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u));
-            epi(v[j], idx);
-            tile[idx] = v[j];
+            for (int j = 0; j < NV; ++j) {
+                const uint32_t off = ((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u);
+                epi(v[j], base ^ off);
+                tile[mb ^ map(off)] = v[j];
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const uint32_t idx = base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u));
+                epi(v[j], idx);
+                tile[idx] = v[j];
+            }
         }
         b = ((b | F) + dstep) & ~F;
     }

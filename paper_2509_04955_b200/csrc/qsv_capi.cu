@@ -859,6 +859,14 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
     if (d.has_relabel) {
         TileOp t{};
         t.kind = QSV_OP_RELABEL;
+        t.k = K;
+        // the permutation itself, for the JIT (a register block may store through it)
+        for (int i = 0; i < K; ++i) {
+            if (i < 8)
+                t.tpos[i] = static_cast<int8_t>(d.relabel[i]);
+            else
+                t.xbit[i - 8] = static_cast<int8_t>(d.relabel[i]);
+        }
         relabel_tab.assign(32, 0);
         relabel_columns(K, d.relabel, relabel_tab.data(), relabel_tab.data() + 16);
         tops.push_back(t);
