@@ -45,8 +45,11 @@ $(LIB)/libqsim.so: $(CPP_OBJ) $(LIB)/libqsv.so
 $(LIB)/qsv: $(PKG)/cpp/tools/qsv.cpp $(LIB)/libqsim.so $(HDRS)
 	$(CXX) $(CXXFLAGS) $< -o $@ -L$(LIB) -lqsim -lqsv -Wl,-rpath,'$$ORIGIN'
 
-oracle/liboracle.so: oracle/oracle.cpp oracle/oracle.h
-	$(CXX) -std=c++20 -O3 -march=x86-64-v3 -fPIC -shared -Wall -Wextra $< -o $@ -lpthread
+# BASELINE.md §3 flags; the shipped build is portable (x86-64-v3), bench.py rebuilds it
+# with -march=native on the GPU box's host (oracle/pyoracle.py native_lib).
+ORACLE_FLAGS := -std=c++20 -O3 -fcx-limited-range -fPIC -shared -Wall -Wextra
+oracle/liboracle.so: oracle/oracle.cpp oracle/gen.cpp oracle/oracle.h
+	$(CXX) $(ORACLE_FLAGS) -march=x86-64-v3 oracle/oracle.cpp oracle/gen.cpp -o $@ -lpthread
 
 ref:
 	@./oracle/build_ref.sh

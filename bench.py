@@ -111,32 +111,89 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_reference_sample(spec: str, budget_s: float, max_gates: int | None = None) -> dict:
-    """Times the CPU restatement of run_local (oracle/) on the full-size state for a
-    bounded prefix of the circuit; returns gates/s over that prefix."""
-    import paper_2509_04955_b200 as pkg
-    from oracle import pyoracle
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
-    c = pkg.Circuit.generate(spec)
-    n, nrec, _ = c.info()
-    threads = pyoracle.threads()
-    amps = np.zeros(1 << n, dtype=np.complex128)
-    amps[0] = 1.0
-    done, t_total, g = 0, 0.0, 0
-    chunk = 1
-    while t_total < budget_s and g < nrec and (max_gates is None or done < max_gates):
-        sl = c.slice(g, min(g + chunk, nrec))
-        t0 = time.perf_counter()
-        amps = pyoracle.run_local(sl, amps, threads)
-        t_total += time.perf_counter() - t0
-        gi = sl.info()[1]
-        done += gi
-        g += gi
-        chunk = min(chunk * 2, 64)
-    return {"value": done / t_total if t_total > 0 else 0.0, "unit": "gates/s", "cores": threads,
-            "kind": "port", "gates": done, "seconds": t_total,
-            "sample": f"first {done} gates of {spec} at full size (2^{n} amplitudes), "
-                      f"oracle run_local (Alg. 3/4 + apply_multi) on {threads} host threads"}
+
+class CpuReference:
+    """The reference's CPU path — the oracle restatement of run_local (Alg. 3/4 +
+    apply_multi), unfused, one pass per gate, on every host thread — on
+    the full-size state, built for this host (-O3 -march=native -fcx-limited-range,
+    BASELINE.md §3).  The circuit comes from the restated generators with the reference's
+    own gate matrices (oracle/gen.cpp + oracle/_ref), so this leg never loads the product
+    libraries.  The state is allocated and first-touched once, by the worker pool; every
+    timed call runs gates in place (no state copy, no export inside the timer)."""
+
+    def __init__(self, spec: str):
+        from oracle import pyoracle
+
+        self.po = pyoracle
+        self.lib = pyoracle.native_lib()
+        self.circ = pyoracle.generate(spec)
+        self.spec = spec
+        self.n = self.circ.n
+        self.threads = int(self.lib.orc_default_threads())
+        self.amps = np.empty(1 << self.n, dtype=np.complex128)
+        self.lib.orc_fill_basis(self.n, self.amps.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint64(0),
+                                self.threads)
+        self.next_gate = 0
+        self.by_class: dict = {}
+
+    def _class(self, i: int) -> str:
+        r = self.circ.recs[i]
+        return "cx" if r.nctrl else "1q"
+
+    def run(self, budget_s: float, min_gates: int = 1) -> dict:
+        """Runs consecutive gates (wrapping to |0> after the last) until budget_s of CPU
+        time and at least min_gates; each gate is timed alone."""
+        done, secs, moved = 0, 0.0, 0.0
+        N = 1 << self.n
+        while secs < budget_s or done < min_gates:
+            if self.next_gate >= self.circ.nr:
+                self.lib.orc_fill_basis(self.n, self.amps.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint64(0),
+                                        self.threads)
+                self.next_gate = 0
+            g = self.circ.slice(self.next_gate, self.next_gate + 1)
+            t0 = time.perf_counter()
+            self.po.run_local(g, self.amps, self.threads, inplace=True, library=self.lib)
+            dt = time.perf_counter() - t0
+            cls = self._class(self.next_gate)
+            # algorithmic bytes: a 1q gate streams the state once (r+w); CX touches the half with control = 1
+            b = 32.0 * N * (0.5 if cls == "cx" else 1.0)
+            c = self.by_class.setdefault(cls, {"gates": 0, "seconds": 0.0, "bytes": 0.0})
+            c["gates"] += 1
+            c["seconds"] += dt
+            c["bytes"] += b
+            moved += b
+            secs += dt
+            done += 1
+            self.next_gate += 1
+        return {"gates": done, "seconds": secs, "bytes": moved}
+
+    def summary(self, gates: int, secs: float, moved: float) -> dict:
+        classes = {k: {"gates": v["gates"], "ms_per_gate": 1e3 * v["seconds"] / v["gates"],
+                       "gbs": v["bytes"] / v["seconds"] / 1e9}
+                   for k, v in self.by_class.items() if v["gates"]}
+        return {"value": gates / secs if secs > 0 else 0.0, "unit": "gates/s", "cores": self.threads,
+                "kind": "port", "gates": gates, "seconds": secs, "gbs": moved / secs / 1e9 if secs else None,
+                "per_class": classes, "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+                "oracle_build": "g++ -O3 -march=native -fcx-limited-range (built on this host)",
+                "sample": f"{gates} consecutive gates of {self.spec} at full size (2^{self.n} amplitudes, "
+                          f"in place, state first-touched once), oracle run_local (Alg. 3/4, one pass per "
+                          f"gate, unfused) on {self.threads} host threads, each gate timed alone"}
+
+
+def cpu_reference_sample(spec: str, budget_s: float, min_gates: int = 1) -> dict:
+    ref = CpuReference(spec)
+    r = ref.run(budget_s, min_gates)
+    return ref.summary(r["gates"], r["seconds"], r["bytes"])
 
 
 def run_reference_arm(args):
@@ -144,23 +201,28 @@ def run_reference_arm(args):
     if rank != 0:
         return
     spec = args.workload
-    # each step: a bounded prefix at full size; warmup steps untimed
-    samples = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference_sample(spec, budget_s=args.ref_budget, max_gates=args.ref_gates)
-        if i >= args.warmup:
-            samples.append(r)
-    gates = sum(s["gates"] for s in samples)
-    secs = sum(s["seconds"] for s in samples)
-    val = gates / secs
+    ref = CpuReference(spec)
+    # one step = the next bounded slice of the same circuit, in place (the state carries
+    # over, as in one long run); warm-up steps are untimed
+    for _ in range(args.warmup):
+        ref.run(args.ref_budget / 4, 1)
+    ref.by_class.clear()
+    gates = secs = moved = 0.0
+    for _ in range(args.steps):
+        r = ref.run(args.ref_budget, 1)
+        gates += r["gates"]
+        secs += r["seconds"]
+        moved += r["bytes"]
+    summ = ref.summary(int(gates), secs, moved)
+    val = summ["value"]
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "gates/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(len(samples), 1),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(args.steps, 1),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128 (f64)",
         "data": "synthetic (seeded generator circuits)",
-        "config": {"workload": spec, "qubits": int(spec.split(":")[1]), "ranks": 1},
-        "cpu_baseline": {"value": val, "unit": "gates/s", "cores": samples[0]["cores"], "kind": "port",
-                         "sample": samples[0]["sample"]},
+        "config": {"workload": spec, "qubits": ref.n, "ranks": 1},
+        "cpu_baseline": {k: summ[k] for k in ("value", "unit", "cores", "kind", "sample", "gbs", "per_class",
+                                              "cpu_model", "nproc", "oracle_build")},
         "e2e": {"value": val, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit_json(line)
@@ -312,9 +374,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-sequential", action="store_true", help="one engine, no copy/compute overlap")
-    ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of CPU work per reference step")
-    ap.add_argument("--ref-gates", type=int, default=None)
-    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds for the cpu_baseline sample")
+    ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per reference step")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds for the cpu_baseline sample")
+    ap.add_argument("--cpu-min-gates", type=int, default=45, help="gates the cpu_baseline sample covers at least")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 untimed warm-up steps
@@ -435,8 +497,9 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_sample(args.workload, budget_s=args.cpu_budget)
-        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = cpu_reference_sample(args.workload, budget_s=args.cpu_budget, min_gates=args.cpu_min_gates)
+        cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "gbs", "per_class", "cpu_model",
+                                   "nproc", "oracle_build")}
 
     if rank != 0:
         if dist is not None:

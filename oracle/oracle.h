@@ -55,10 +55,25 @@ int orc_apply_multi(int n, double* amps, int k, const int* targets, int nctrl, c
  * reference does (1q -> Alg. 3, 1q+1 control -> Alg. 4, else apply_multi). */
 int orc_run_local(int n, const orc_gate* gates, int64_t ngates, const double* pool, double* amps,
                   int threads);
+/* The same run_local as a cache-blocked schedule: maximal runs of consecutive
+ * gates whose qubits fit in block_bits bits are applied block by block
+ * (gather 2^block_bits amplitudes, the run's gates in program order, scatter).
+ * Bitwise equal to orc_run_local; used to check full-size states in tests. */
+int orc_run_local_blocked(int n, const orc_gate* gates, int64_t ngates, const double* pool, double* amps,
+                          int threads, int block_bits);
 /* dense_oracle: every gate embedded as an explicit 2^n x 2^n
  * matrix (row by row) and multiplied into the state; n <= 12. */
 int orc_dense_oracle(int n, const orc_gate* gates, int64_t ngates, const double* pool,
                      const double* in, double* out);
+/* Workload generators restated for the reference arm (oracle/gen.cpp): the
+ * spec's gates as mnemonic instructions (code = ORC_*, q0 = first qubit /
+ * control, q1 = target of a two-qubit gate or -1, params = angle).  Returns the
+ * gate count (fills the arrays when cap >= count), -1 on a bad spec. */
+enum { ORC_H = 0, ORC_RX = 1, ORC_RY = 2, ORC_RZ = 3, ORC_CX = 4, ORC_CP = 5 };
+int64_t orc_generate(const char* spec, int* n, int32_t* codes, int32_t* q0, int32_t* q1, double* params,
+                     int64_t cap);
+/* |index> into a 2^n buffer, zero-filled by the worker pool (parallel first touch). */
+int orc_fill_basis(int n, double* amps, uint64_t index, int threads);
 /* Hardware threads the oracle uses by default. */
 int orc_default_threads(void);
 

@@ -135,3 +135,46 @@ def test_worker_count_bitwise_determinism():  # SPEC:111, acceptance #10
 def test_dense_oracle_scale_guard():
     with pytest.raises(RuntimeError):
         O.dense_oracle(pkg.Circuit.empty(13).add("h", [0]))
+
+
+def _flat(circ):
+    """(targets, controls, matrix) per gate record of an exported circuit."""
+    n, recs, nr, pool = circ.export()
+    out = []
+    for i in range(nr):
+        r = recs[i]
+        d = 1 << r.arity
+        m = pool[r.mat_off:r.mat_off + d * d]
+        out.append((tuple(r.targets[:r.arity]), tuple(r.controls[:r.nctrl]), m.tobytes()))
+    return n, out
+
+
+@pytest.mark.parametrize("spec", ["qft:9", "qaoa:8:2:5", "hea:7:3:2", "random:9:6:4", "uccsd:8:300:3"])
+def test_generator_restatement_matches_product(spec):
+    """oracle/gen.cpp (the reference arm's circuits, built without the product
+    libraries) is gate-for-gate and bit-for-bit the product generator."""
+    n0, a = _flat(pkg.Circuit.generate(spec))
+    n1, b = _flat(O.generate(spec))
+    assert n0 == n1 and len(a) == len(b)
+    assert a == b
+
+
+@pytest.mark.parametrize("spec,bits", [("random:14:8:3", 8), ("uccsd:13:400:2", 6), ("qft:12", 5),
+                                       ("hea:12:3:1", 10)])
+def test_blocked_run_local_bitwise(spec, bits):
+    """The cache-blocked schedule (full-size parity checks) is bitwise the pooled run_local."""
+    c = O.generate(spec)
+    a = rand_state(c.n, 7)
+    ref = O.run_local(c, a)
+    got = O.run_local(c, a, blocked=True, block_bits=bits)
+    assert np.array_equal(ref, got)
+
+
+def test_inplace_run_local_and_fill_basis():
+    c = O.generate("random:12:4:1")
+    a = np.empty(1 << 12, dtype=np.complex128)
+    O.fill_basis(a, 5)
+    assert a[5] == 1 and np.count_nonzero(a) == 1
+    ref = O.run_local(c, a)
+    out = O.run_local(c, a, inplace=True)
+    assert out is a and np.array_equal(a, ref)
