@@ -55,8 +55,10 @@ def random_unitary_circuit(n, ngates, seed, kmax=3, ctrl=True):
     return c
 
 
-def qft_basis_expected(n, x):
-    y = np.arange(1 << n, dtype=np.uint64)
+def qft_basis_expected(n, x, offset=0, count=None):
+    """QFT|x> amplitudes [offset, offset + count) (all of them by default)."""
+    count = (1 << n) - offset if count is None else count
+    y = np.arange(offset, offset + count, dtype=np.uint64)
     ph = (np.uint64(x) * y) & np.uint64((1 << n) - 1)
     return np.exp(2j * np.pi * ph.astype(np.float64) / (1 << n)) / math.sqrt(1 << n)
 

@@ -9,6 +9,7 @@ import pytest
 
 import paper_2509_04955_b200 as pkg
 from oracle import pyoracle as O
+from tests.helpers import qft_basis_expected
 
 pytestmark = pytest.mark.gpu
 
@@ -72,11 +73,50 @@ def test_four_gpu_vs_oracle():
         assert rep.ranks == 4
 
 
-def test_qft_large_distributed_analytic(two):
-    # 30 qubits over 2 GPUs from |0..0>: analytic uniform answer (checked on host)
-    c = pkg.Circuit.generate("qft:28")
-    got, rep = run_dist(c, 1, 20, 2)
-    assert np.abs(got - 2.0 ** (-14)).max() <= 1e-10
+def _qft_of_basis(n, x):
+    """X on the set bits of x, then QFT: the distributed run starts from |0...0>."""
+    c = pkg.Circuit.empty(n)
+    for q in range(n):
+        if x >> q & 1:
+            c.add("x", [q])
+    return c.concat(pkg.Circuit.generate(f"qft:{n}"))
+
+
+@pytest.mark.parametrize("n,m", [(28, 1), (29, 2)])
+def test_qft_large_distributed_basis_analytic(two, n, m):
+    """QFT|x> = e^{2 pi i x y / 2^n} / 2^{n/2} on every amplitude (sensitive to
+    the CP angles and the reversal layer, unlike QFT|0>), over 2 and 4 GPUs."""
+    if ngpus() < (1 << m):
+        pytest.skip(f"needs {1 << m} GPUs")
+    x = 0x2A5A5A5 & ((1 << n) - 1)
+    got, rep = run_dist(_qft_of_basis(n, x), m, 22, 2)
+    assert rep.ranks == 1 << m and rep.swaps >= 1
+    worst = 0.0
+    step = 1 << 24
+    for off in range(0, 1 << n, step):
+        worst = max(worst, float(np.abs(got[off:off + step] - qft_basis_expected(n, x, off, step)).max()))
+    assert worst <= 1e-10
+
+
+DETERMINISTIC = pkg.PlanOptions(fusion=False, list_schedule=False, relabel=0, register_blocks=False)
+
+
+@pytest.mark.parametrize("spec", ["random:20:10:2", "qft:19", "hea:19:3:4", "uccsd:18:600:3"])
+def test_cross_p_bitwise(two, spec):
+    """fusion runs before partitioning and the fused block sequence is applied in
+    the same order on every P, so the 1-, 2- and 4-GPU results are bitwise equal."""
+    fused = pkg.Circuit.generate(spec).fused(pkg.PlanOptions())
+    e = pkg.Engine(fused, DETERMINISTIC)
+    e.set_basis(0)
+    e.run()
+    e.sync()
+    one = e.download()
+    e.close()
+    for m in (1, 2):
+        if ngpus() < (1 << m):
+            continue
+        got, _ = run_dist(fused, m, 12, 2, DETERMINISTIC)
+        assert np.array_equal(got, one), f"P={1 << m}: max diff {np.abs(got - one).max():.3e}"
 
 
 @pytest.mark.parametrize("mode", [{"QSV_SWAP_MODE": "nccl"}, {"QSV_OVERLAP": "1"},

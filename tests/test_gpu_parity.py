@@ -239,3 +239,42 @@ def test_mirror_full_size(spec):  # configs[1..3] shapes at full size
 def test_mirror_hea33_128GiB():  # configs[3]: 33 qubits, 128 GiB on one B200
     err0, nerr = _mirror_check("hea:33:5:4")
     assert err0 <= 1e-10 and nerr <= 1e-12
+
+
+@pytest.mark.parametrize("relabel", [1, 2])
+def test_uccsd_full_ladder_vs_oracle(relabel):  # configs[2]: the whole ~1e5-CX ladder, oracle-checkable n
+    c = pkg.Circuit.generate("uccsd:20:100000:3")
+    ref = O.run_local(c)
+    got, norm = run_gpu(c, None, pkg.PlanOptions(relabel=relabel))
+    assert np.abs(got - ref).max() <= TOL
+    assert abs(norm - 1) <= NORM_TOL
+
+
+def test_uccsd28_full_ladder_norm_and_mirror():  # configs[2] at its stated size: 28 qubits, ~1e5 CX
+    c = pkg.Circuit.generate("uccsd:28:100000:3")
+    e = pkg.Engine(c)
+    e.set_basis(0)
+    e.run()
+    assert abs(e.norm_sq() - 1) <= NORM_TOL
+    e.close()
+    err0, nerr = _mirror_check("uccsd:28:100000:3")
+    assert err0 <= 1e-10 and nerr <= 1e-12
+
+
+def test_random30_full_size_vs_oracle():  # configs[1] at full size against the CPU oracle (16 GiB)
+    c = pkg.Circuit.generate("random:30:20:2")
+    n = 30
+    e = pkg.Engine(c)
+    e.set_basis(0)
+    e.run()
+    e.sync()
+    assert abs(e.norm_sq() - 1) <= NORM_TOL
+    ref = np.empty(1 << n, dtype=np.complex128)
+    O.fill_basis(ref, 0)
+    O.run_local(O.generate("random:30:20:2"), ref, inplace=True, library=O.native_lib())
+    worst = 0.0
+    step = 1 << 24
+    for off in range(0, 1 << n, step):  # compared on the device, 256 MiB slices
+        worst = max(worst, e.max_abs_diff(ref[off:off + step], off))
+    e.close()
+    assert worst <= TOL
