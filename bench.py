@@ -35,7 +35,21 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 HBM_FALLBACK_GBS = 6650.0
-F64_NOMINAL_TFLOPS = 37.0  # B200 FP64 (DFMA = DMMA) nominal; not in MEASURED_PEAKS.json
+F64_NOMINAL_TFLOPS = 37.0  # B200 FP64 datasheet figure; used only when the measured file is absent
+
+
+def load_f64_peak() -> tuple[float, str]:
+    """The FP64 peak the pass roofline uses: max(DFMA, DMMA) measured by tools/fp64_peak.cu
+    on a B200 of this pool (profiles/r02_fp64_peak.json, 37.0 / 37.1 TF at 1965 MHz)."""
+    p = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return max(float(d["dfma_tflops"]), float(d["dmma_tflops"])), \
+            "measured (profiles/r02_fp64_peak.json: tools/fp64_peak.cu, DFMA %.1f / DMMA %.1f TF)" % (
+                d["dfma_tflops"], d["dmma_tflops"])
+    except Exception:
+        return F64_NOMINAL_TFLOPS, "nominal B200 datasheet (profiles/r02_fp64_peak.json absent)"
 METRIC = "gates/s (circuit time & HBM GB/s reported alongside)"
 
 
@@ -471,9 +485,10 @@ def main():
     pass_bytes = [s["hbm_bytes"] for s in steps_info if s["kind"] == "pass"]
     pass_flops = [s["flops"] for s in steps_info if s["kind"] == "pass"]
     hbm_peak, hbm_src = load_peaks()
+    f64_peak, f64_src = load_f64_peak()
     avg_pass_ms = sum(pass_ms) / max(len(pass_ms), 1)
     achieved = (sum(pass_bytes) / max(len(pass_bytes), 1)) / (avg_pass_ms / 1e3) / 1e9 if pass_ms else 0.0
-    t_roof = sum(max(b / (hbm_peak * 1e9), f / (F64_NOMINAL_TFLOPS * 1e12)) for b, f in zip(pass_bytes, pass_flops))
+    t_roof = sum(max(b / (hbm_peak * 1e9), f / (f64_peak * 1e12)) for b, f in zip(pass_bytes, pass_flops))
     nvl = sum(s["nvl_bytes"] for s in steps_info)
     t_roof += nvl / 770e9
     norm = eng.norm_sq()
@@ -537,7 +552,7 @@ def main():
             "algorithmic_bytes_per_launch": sum(pass_bytes) / max(len(pass_bytes), 1),
             "avg_launch_ms": avg_pass_ms,
             "circuit_roofline_time_s": t_roof, "circuit_roofline_frac": t_roof / (ms_step / 1e3),
-            "f64_peak_tflops": F64_NOMINAL_TFLOPS, "f64_peak_source": "nominal B200 datasheet",
+            "f64_peak_tflops": f64_peak, "f64_peak_source": f64_src,
             "achieved_tflops": sum(pass_flops) / (sum(pass_ms) / 1e3) / 1e12 if pass_ms else None,
         },
         "swap_ms_total": sum(swap_ms) if swap_ms else 0.0,

