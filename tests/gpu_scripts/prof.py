@@ -9,5 +9,6 @@ prof = e.profile()
 st = e.steps()
 for i, (p, s) in enumerate(zip(prof, st)):
     if i < 200:
-        print(i, "%.3f ms" % p, s["nops"], "%.1f GB/s" % (s["hbm_bytes"] / p / 1e6))
+        print(i, "%.3f ms" % p, s["nops"], "%.1f GB/s" % (s["hbm_bytes"] / p / 1e6),
+              "%.2f TF" % (s.get("flops", 0) / p / 1e9), "%.0f flop/amp" % (s.get("flops", 0) / (s["hbm_bytes"] / 32)))
 print("total", sum(prof))
