@@ -75,6 +75,15 @@ void* qsv_ctx_stream(qsv_ctx* ctx);
 int qsv_ctx_staging_bytes(qsv_ctx* ctx, size_t* out);
 /* Blocks until all work queued on the context has finished. */
 int qsv_sync(qsv_ctx* ctx);
+/* Collective failure semantics ("any collective error aborts all ranks
+ * with diagnostics").  qsv_ctx_abort tears down the context's communicator
+ * (ncclCommAbort) from any thread, so every rank blocked in a swap or barrier
+ * returns QSV_E_NCCL instead of waiting for a peer that will never arrive; the
+ * reason is reported by every later call on the context.  Waits on multi-rank
+ * contexts also poll ncclCommGetAsyncError and abort after QSV_COLL_TIMEOUT_S
+ * seconds (default 900).  qsv_ctx_aborted reports whether the context was aborted. */
+int qsv_ctx_abort(qsv_ctx* ctx, const char* reason);
+int qsv_ctx_aborted(qsv_ctx* ctx, int* out);
 /* Thread-local description of the last failure on this thread. */
 const char* qsv_last_error(void);
 

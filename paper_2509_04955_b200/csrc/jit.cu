@@ -30,6 +30,7 @@
 #include <sstream>
 #include <string>
 #include <sys/stat.h>
+#include <unistd.h>
 #include <thread>
 #include <vector>
 
@@ -519,21 +520,20 @@ void mkdirs(const std::string& p) {
 }
 
 // Compiles one translation unit to a cubin (or loads it from the cache).
-bool compile_unit(const std::string& src, std::vector<char>& cubin, std::string& err) {
+const char* const kJitOpts[4] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-diag-suppress=177,550"};
+std::string unit_cache_path(const std::string& src);
+
+// Compiles one translation unit to a cubin (or loads it from the cache unless
+// use_cache is false: a cached cubin the driver rejected is recompiled).
+bool compile_unit(const std::string& src, std::vector<char>& cubin, std::string& err, bool use_cache = true) {
     if (const char* dump = std::getenv("QSV_JIT_DUMP")) {  // debugging: keep the generated source
         char name[64];
         std::snprintf(name, sizeof(name), "/qsv_%016llx.cu", static_cast<unsigned long long>(fnv1a(src)));
         std::ofstream(std::string(dump) + name) << src;
     }
-    static const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-diag-suppress=177,550"};
-    std::string key = src;
-    for (const char* op : opts)
-        key += op;
     const std::string dir = cache_dir();
-    char hex[32];
-    std::snprintf(hex, sizeof(hex), "%016llx", static_cast<unsigned long long>(fnv1a(key)));
-    const std::string path = dir + "/qsv_" + hex + ".cubin";
-    {
+    const std::string path = unit_cache_path(src);
+    if (use_cache) {
         std::ifstream in(path, std::ios::binary);
         if (in) {
             cubin.assign(std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>());
@@ -543,6 +543,7 @@ bool compile_unit(const std::string& src, std::vector<char>& cubin, std::string&
     }
     const Nvrtc& n = nvrtc();
     nvrtcProgram prog;
+    static const char* opts[] = {kJitOpts[0], kJitOpts[1], kJitOpts[2], kJitOpts[3]};
     if (n.create(&prog, src.c_str(), "qsv_jit.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
         err = "nvrtcCreateProgram failed";
         return false;
@@ -563,13 +564,30 @@ bool compile_unit(const std::string& src, std::vector<char>& cubin, std::string&
     n.cubin(prog, cubin.data());
     n.destroy(&prog);
     mkdirs(dir);
-    const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<uintptr_t>(&cubin));
+    // unique per process and thread (several ranks on one node share the cache);
+    // only a completely written file is renamed into place
+    std::ostringstream tn;
+    tn << path << ".tmp." << getpid() << "." << std::this_thread::get_id();
+    const std::string tmp = tn.str();
+    bool good;
     {
         std::ofstream out(tmp, std::ios::binary);
         out.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
+        out.flush();
+        good = static_cast<bool>(out);
     }
-    std::rename(tmp.c_str(), path.c_str());
+    if (!good || std::rename(tmp.c_str(), path.c_str()) != 0)
+        std::remove(tmp.c_str());  // the cache is an optimisation: the cubin in memory is fine
     return true;
+}
+
+std::string unit_cache_path(const std::string& src) {
+    std::string key = src;
+    for (const char* op : kJitOpts)
+        key += op;
+    char hex[32];
+    std::snprintf(hex, sizeof(hex), "%016llx", static_cast<unsigned long long>(fnv1a(key)));
+    return cache_dir() + "/qsv_" + hex + ".cubin";
 }
 
 } // namespace
@@ -624,7 +642,8 @@ constexpr int kKernelsPerUnit = 6;
 
 // NVRTC-compiles the kernels of `jp` in translation units of kKernelsPerUnit,
 // concurrently (no device needed).
-bool compile_kernels(const JitPlan& jp, std::vector<std::vector<char>>& cubins, std::string& err) {
+bool compile_kernels(const JitPlan& jp, std::vector<std::vector<char>>& cubins, std::string& err,
+                     std::vector<std::string>* sources = nullptr) {
     const int nk = static_cast<int>(jp.bodies.size());
     const int nunits = (nk + kKernelsPerUnit - 1) / kKernelsPerUnit;
     std::vector<std::string> srcs(nunits);
@@ -651,6 +670,8 @@ bool compile_kernels(const JitPlan& jp, std::vector<std::vector<char>>& cubins, 
             err = errs[u];
             return false;
         }
+    if (sources)
+        *sources = std::move(srcs);
     return true;
 }
 
@@ -692,8 +713,9 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
     const int nunits = (nk + per_unit - 1) / per_unit;
     const std::vector<int>& kernel_k = jp.kernel_k;
     std::vector<std::vector<char>> cubins;
+    std::vector<std::string> srcs;
     std::string err;
-    if (!compile_kernels(jp, cubins, err)) {
+    if (!compile_kernels(jp, cubins, err, &srcs)) {
         prog->jit_of_step.assign(prog->steps.size(), -1);
         set_error("qsv_program_jit: " + err);
         return QSV_E_CUDA;
@@ -706,9 +728,13 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
     for (int u = 0; u < nunits; ++u) {
         CUmodule mod;
         if (d.module_load(&mod, cubins[u].data()) != CUDA_SUCCESS) {
-            prog->jit_of_step.assign(prog->steps.size(), -1);
-            set_error("qsv_program_jit: cuModuleLoadData failed");
-            return QSV_E_CUDA;
+            // a stale or damaged cache entry: drop it and compile this unit afresh
+            std::remove(unit_cache_path(srcs[u]).c_str());
+            if (!compile_unit(srcs[u], cubins[u], err, false) || d.module_load(&mod, cubins[u].data()) != CUDA_SUCCESS) {
+                prog->jit_of_step.assign(prog->steps.size(), -1);
+                set_error("qsv_program_jit: cuModuleLoadData failed" + (err.empty() ? std::string() : ": " + err));
+                return QSV_E_CUDA;
+            }
         }
         prog->jit_modules.push_back(mod);
         for (int k = u * per_unit; k < std::min(nk, (u + 1) * per_unit); ++k) {

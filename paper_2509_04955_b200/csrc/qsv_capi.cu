@@ -10,6 +10,8 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
+#include <chrono>
 #include <vector>
 
 namespace qsv {
@@ -269,16 +271,111 @@ extern "C" int qsv_ctx_create(int device, int rank, int nranks, const void* comm
     QSV_CUDA(cudaEventCreateWithFlags(&ctx->ev_b, cudaEventDisableTiming));
     QSV_CUDA(cudaMallocHost(&ctx->h_result, 4 * sizeof(double)));
     if (nranks > 1) {
+        // local allocations first; the init is joined whatever their outcome (the peers
+        // are already inside it) and a rank whose allocations failed aborts right after,
+        // so the others see an async error instead of waiting forever
+        const cudaError_t ea = cudaMalloc(&ctx->d_coll, 128 * static_cast<size_t>(nranks) + 64);
+        const cudaError_t eb = ea == cudaSuccess ? cudaMalloc(&ctx->d_sync, 2 * sizeof(double)) : ea;
+        if (eb == cudaSuccess)
+            cudaMemset(ctx->d_sync, 0, 2 * sizeof(double));
+        cudaGetLastError();
         ncclUniqueId id;
         std::memcpy(&id, comm_id, sizeof(id));
         ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, id, rank);
-        if (r != ncclSuccess) {
-            set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        if (r != ncclSuccess || ea != cudaSuccess || eb != cudaSuccess) {
+            const std::string why = r != ncclSuccess ? std::string("ncclCommInitRank: ") + ncclGetErrorString(r)
+                                                     : std::string("collective scratch cudaMalloc: ") +
+                                                           cudaGetErrorString(ea != cudaSuccess ? ea : eb);
+            if (r == ncclSuccess)
+                ncclCommAbort(ctx->comm);
+            if (ctx->d_coll) cudaFree(ctx->d_coll);
+            if (ctx->d_sync) cudaFree(ctx->d_sync);
+            cudaFreeHost(ctx->h_result);
+            set_error("qsv_ctx_create (rank " + std::to_string(rank) + "): " + why);
             delete ctx;
-            return QSV_E_NCCL;
+            return r != ncclSuccess ? QSV_E_NCCL : QSV_E_NOMEM;
         }
     }
     *out = ctx;
+    return QSV_OK;
+}
+
+namespace qsv {
+
+void abort_comm(qsv_ctx* ctx, const std::string& why) {
+    if (ctx->aborted.exchange(1) == 0)
+        ctx->abort_reason = why;
+    if (ctx->comm && ctx->comm_aborted.exchange(1) == 0)
+        ncclCommAbort(ctx->comm);  // unblocks every NCCL kernel of this rank
+}
+
+int check_aborted(qsv_ctx* ctx, const char* what) {
+    if (!ctx->aborted.load())
+        return QSV_OK;
+    set_error(std::string(what) + " (rank " + std::to_string(ctx->rank) + "): collective aborted: " +
+              ctx->abort_reason);
+    return QSV_E_NCCL;
+}
+
+int wait_stream(qsv_ctx* ctx, cudaStream_t stream, const char* what) {
+    if (ctx->nranks < 2 || ctx->comm == nullptr) {
+        const cudaError_t e = cudaStreamSynchronize(stream);
+        if (e != cudaSuccess) {
+            set_error(std::string(what) + ": " + cudaGetErrorString(e));
+            return QSV_E_CUDA;
+        }
+        return QSV_OK;
+    }
+    static const double timeout_s = [] {
+        const char* v = std::getenv("QSV_COLL_TIMEOUT_S");
+        const double t = v ? std::atof(v) : 900.0;
+        return t > 0 ? t : 900.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    int sleep_us = 20;
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(stream);
+        if (q == cudaSuccess)
+            return check_aborted(ctx, what);
+        if (q != cudaErrorNotReady) {
+            abort_comm(ctx, std::string("CUDA error on rank ") + std::to_string(ctx->rank) + ": " +
+                                cudaGetErrorString(q));
+            set_error(std::string(what) + " (rank " + std::to_string(ctx->rank) + "): " + cudaGetErrorString(q));
+            return QSV_E_CUDA;
+        }
+        if (ctx->aborted.load()) {
+            abort_comm(ctx, ctx->abort_reason);  // make sure the comm is torn down too
+            // the NCCL kernels exit after the abort; let the stream drain
+            cudaStreamSynchronize(stream);
+            cudaGetLastError();
+            return check_aborted(ctx, what);
+        }
+        if (!ctx->comm_aborted.load()) {
+            ncclResult_t ae = ncclSuccess;
+            if (ncclCommGetAsyncError(ctx->comm, &ae) == ncclSuccess && ae != ncclSuccess && ae != ncclInProgress)
+                abort_comm(ctx, std::string("NCCL async error on rank ") + std::to_string(ctx->rank) + ": " +
+                                    ncclGetErrorString(ae));
+        }
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > timeout_s && !ctx->aborted.load())
+            abort_comm(ctx, "rank " + std::to_string(ctx->rank) + " waited " + std::to_string(static_cast<int>(el)) +
+                                " s in " + what + " (QSV_COLL_TIMEOUT_S): a peer rank is gone or hung");
+        std::this_thread::sleep_for(std::chrono::microseconds(sleep_us));
+        sleep_us = std::min(sleep_us * 2, 1000);
+    }
+}
+
+} // namespace qsv
+
+extern "C" int qsv_ctx_abort(qsv_ctx* ctx, const char* reason) {
+    QSV_REQUIRE(ctx != nullptr, "qsv_ctx_abort: null context");
+    qsv::abort_comm(ctx, reason ? reason : "aborted by the caller");
+    return QSV_OK;
+}
+
+extern "C" int qsv_ctx_aborted(qsv_ctx* ctx, int* out) {
+    QSV_REQUIRE(ctx != nullptr && out != nullptr, "qsv_ctx_aborted: null argument");
+    *out = ctx->aborted.load();
     return QSV_OK;
 }
 
@@ -286,13 +383,17 @@ extern "C" int qsv_ctx_destroy(qsv_ctx* ctx) {
     if (!ctx)
         return QSV_OK;
     cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    if (ctx->comm)
+    if (ctx->aborted.load())
+        cudaStreamSynchronize(ctx->stream);  // NCCL kernels have exited after the abort
+    else
+        qsv::wait_stream(ctx, ctx->stream, "qsv_ctx_destroy");
+    if (ctx->comm && !ctx->comm_aborted.load())
         ncclCommDestroy(ctx->comm);
     if (ctx->d_partials) cudaFree(ctx->d_partials);
     if (ctx->d_stage) cudaFree(ctx->d_stage);
     if (ctx->d_scratch) cudaFree(ctx->d_scratch);
     if (ctx->d_sync) cudaFree(ctx->d_sync);
+    if (ctx->d_coll) cudaFree(ctx->d_coll);
     if (ctx->h_result) cudaFreeHost(ctx->h_result);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
@@ -314,8 +415,7 @@ extern "C" void* qsv_ctx_stream(qsv_ctx* ctx) { return ctx ? static_cast<void*>(
 extern "C" int qsv_sync(qsv_ctx* ctx) {
     QSV_REQUIRE(ctx != nullptr, "qsv_sync: null context");
     QSV_CUDA(cudaSetDevice(ctx->device));
-    QSV_CUDA(cudaStreamSynchronize(ctx->stream));
-    return QSV_OK;
+    return qsv::wait_stream(ctx, ctx->stream, "qsv_sync");
 }
 
 extern "C" const char* qsv_last_error(void) { return qsv::t_err.c_str(); }
@@ -1363,6 +1463,8 @@ extern "C" int qsv_program_run(qsv_state* st, qsv_program* prog) {
     QSV_REQUIRE(st->ctx == prog->ctx, "qsv_program_run: state and program belong to different contexts");
     QSV_REQUIRE(st->n_local == prog->n_local, "qsv_program_run: state size differs from the program's");
     qsv_ctx* ctx = st->ctx;
+    if (int rc = qsv::check_aborted(ctx, "qsv_program_run"); rc != QSV_OK)
+        return rc;
     QSV_CUDA(cudaSetDevice(ctx->device));
     if (prog->has_collective || prog->steps.size() < 4)
         return enqueue_steps(st, prog, nullptr);

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <cstdint>
 #include <map>
 #include <string>
@@ -61,6 +62,14 @@ struct qsv_ctx {
     size_t scratch_bytes = 0;
     // pairwise barrier tokens of the P2P swap (2 doubles)
     double* d_sync = nullptr;
+    // collective scratch (peer-handle exchange: 128 B per rank + a flag), allocated
+    // before the communicator so that no rank leaves a collective early
+    unsigned char* d_coll = nullptr;
+    // failure semantics: set by qsv_ctx_abort (any thread) or by a failed
+    // wait; once set, every later call on this context fails with QSV_E_NCCL
+    std::atomic<int> aborted{0};
+    std::atomic<int> comm_aborted{0};
+    std::string abort_reason;
 };
 
 struct qsv_state {
@@ -136,4 +145,13 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf,
 // Collective on first use: maps the peers' shards; true when swap g will use NVLink P2P.
 bool p2p_swap_ready(qsv_state* st, int g);
 void join_swap(qsv_ctx* ctx);
+// Waits for `stream` on a multi-rank context without hanging on a dead peer: polls
+// the stream, the context's abort flag and ncclCommGetAsyncError, and aborts the
+// communicator (ncclCommAbort) after QSV_COLL_TIMEOUT_S seconds (default 900).
+// Single-rank contexts synchronize directly.  Returns QSV_OK or QSV_E_NCCL/QSV_E_CUDA.
+int wait_stream(qsv_ctx* ctx, cudaStream_t stream, const char* what);
+// Aborts the communicator once (safe from any thread) and records `why`.
+void abort_comm(qsv_ctx* ctx, const std::string& why);
+// QSV_E_NCCL with the abort reason when the context was aborted, else QSV_OK.
+int check_aborted(qsv_ctx* ctx, const char* what);
 } // namespace qsv

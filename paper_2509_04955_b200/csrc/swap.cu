@@ -145,8 +145,10 @@ struct PeerInfo {
 };
 static_assert(sizeof(PeerInfo) == 128, "PeerInfo is exchanged as 128 bytes");
 
-// Collective (all ranks): maps every peer's shard into this process.
-void exchange_peers(qsv_state* st) {
+// Collective (all ranks): maps every peer's shard into this process.  Every rank
+// joins both collectives whatever its local state (a failure only lowers its `ok`
+// flag, which the ncclMin all-reduce combines), so no rank is left waiting.
+int exchange_peers(qsv_state* st) {
     qsv_ctx* ctx = st->ctx;
     st->peers_ready = true;
     st->peer_amps.assign(ctx->nranks, nullptr);
@@ -157,20 +159,25 @@ void exchange_peers(qsv_state* st) {
     mine.ptr = reinterpret_cast<uint64_t>(st->amps);
     mine.pid = static_cast<int32_t>(getpid());
     mine.device = ctx->device;
-    void* d_info = nullptr;
-    if (cudaMalloc(&d_info, sizeof(PeerInfo) * ctx->nranks) != cudaSuccess)
-        return;
+    unsigned char* d_info = ctx->d_coll;  // 128 B per rank, then the flag
+    int* d_flag = reinterpret_cast<int*>(d_info + sizeof(PeerInfo) * ctx->nranks);
     std::vector<PeerInfo> all(ctx->nranks);
-    bool ok = cudaMemcpy(static_cast<char*>(d_info) + sizeof(PeerInfo) * ctx->rank, &mine, sizeof(PeerInfo),
-                         cudaMemcpyHostToDevice) == cudaSuccess;
-    ok = ok && ncclAllGather(static_cast<char*>(d_info) + sizeof(PeerInfo) * ctx->rank, d_info, sizeof(PeerInfo),
-                             ncclChar, ctx->comm, ctx->comm_stream) == ncclSuccess;
-    ok = ok && cudaStreamSynchronize(ctx->comm_stream) == cudaSuccess;
-    ok = ok && cudaMemcpy(all.data(), d_info, sizeof(PeerInfo) * ctx->nranks, cudaMemcpyDeviceToHost) == cudaSuccess;
-    cudaFree(d_info);
-    if (!ok)
-        return;
-    for (int q = 0; q < ctx->nranks; ++q) {
+    bool local_ok = cudaMemcpy(d_info + sizeof(PeerInfo) * ctx->rank, &mine, sizeof(PeerInfo),
+                               cudaMemcpyHostToDevice) == cudaSuccess;
+    cudaGetLastError();
+    ncclResult_t r = ncclAllGather(d_info + sizeof(PeerInfo) * ctx->rank, d_info, sizeof(PeerInfo), ncclChar,
+                                   ctx->comm, ctx->comm_stream);
+    if (r != ncclSuccess) {
+        abort_comm(ctx, std::string("ncclAllGather: ") + ncclGetErrorString(r));
+        return check_aborted(ctx, "qsv_swap: peer handle exchange");
+    }
+    int rc = wait_stream(ctx, ctx->comm_stream, "qsv_swap: peer handle exchange");
+    if (rc != QSV_OK)
+        return rc;
+    local_ok = local_ok &&
+               cudaMemcpy(all.data(), d_info, sizeof(PeerInfo) * ctx->nranks, cudaMemcpyDeviceToHost) == cudaSuccess;
+    cudaGetLastError();
+    for (int q = 0; q < ctx->nranks && local_ok; ++q) {
         if (q == ctx->rank)
             continue;
         const PeerInfo& pi = all[q];
@@ -197,17 +204,26 @@ void exchange_peers(qsv_state* st) {
         }
     }
     // all ranks must take the same path: P2P only if every rank mapped every peer
-    int ok_local = 1;
+    int ok_local = local_ok ? 1 : 0;
     for (int q = 0; q < ctx->nranks; ++q)
         ok_local &= (q == ctx->rank || st->peer_amps[q] != nullptr) ? 1 : 0;
-    int* d_flag = nullptr;
     int ok_all = 0;
-    if (cudaMalloc(&d_flag, sizeof(int)) == cudaSuccess) {
-        cudaMemcpy(d_flag, &ok_local, sizeof(int), cudaMemcpyHostToDevice);
-        if (ncclAllReduce(d_flag, d_flag, 1, ncclInt32, ncclMin, ctx->comm, ctx->comm_stream) == ncclSuccess &&
-            cudaStreamSynchronize(ctx->comm_stream) == cudaSuccess)
-            cudaMemcpy(&ok_all, d_flag, sizeof(int), cudaMemcpyDeviceToHost);
-        cudaFree(d_flag);
+    if (cudaMemcpy(d_flag, &ok_local, sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        // the flag cannot be set: contribute 0 through a device-side memset instead
+        cudaMemsetAsync(d_flag, 0, sizeof(int), ctx->comm_stream);
+    }
+    r = ncclAllReduce(d_flag, d_flag, 1, ncclInt32, ncclMin, ctx->comm, ctx->comm_stream);
+    if (r != ncclSuccess) {
+        abort_comm(ctx, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+        return check_aborted(ctx, "qsv_swap: peer map agreement");
+    }
+    rc = wait_stream(ctx, ctx->comm_stream, "qsv_swap: peer map agreement");
+    if (rc != QSV_OK)
+        return rc;
+    if (cudaMemcpy(&ok_all, d_flag, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        ok_all = 0;
     }
     if (!ok_all) {
         for (int q = 0; q < ctx->nranks; ++q)
@@ -216,6 +232,7 @@ void exchange_peers(qsv_state* st) {
         st->peer_amps.assign(ctx->nranks, nullptr);
         st->peer_ipc.assign(ctx->nranks, 0);
     }
+    return QSV_OK;
 }
 
 // Pairwise barrier with `peer` on the comm stream (an 8-byte grouped send/recv).
@@ -250,8 +267,8 @@ bool p2p_swap_ready(qsv_state* st, int g) {
     qsv_ctx* ctx = st->ctx;
     if (!p2p_mode() || ctx->nranks < 2 || ctx->comm == nullptr)
         return false;
-    if (!st->peers_ready)
-        exchange_peers(st);  // collective: every rank reaches the same swap
+    if (!st->peers_ready && exchange_peers(st) != QSV_OK)  // collective: every rank reaches the same swap
+        return false;
     const int l = st->n_local;
     const int peer = ctx->rank ^ (1 << (g - l));
     return st->peer_amps.size() == static_cast<size_t>(ctx->nranks) && peer < ctx->nranks && st->peer_amps[peer];
@@ -280,9 +297,14 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
     const uint64_t a = static_cast<uint64_t>((ctx->rank >> (g - l)) & 1);
     const uint64_t sendbit = a ^ 1ull;
 
+    if (int rc = check_aborted(ctx, "qsv_swap"); rc != QSV_OK)
+        return rc;
     if (p2p_mode()) {
-        if (!st->peers_ready)
-            exchange_peers(st);  // collective: every rank reaches its first swap
+        if (!st->peers_ready) {
+            const int rc = exchange_peers(st);  // collective: every rank reaches its first swap
+            if (rc != QSV_OK)
+                return rc;
+        }
         // every rank must agree on the mode: P2P only when both sides mapped each other,
         // which holds symmetrically on one NVSwitch box (checked per pair below)
     }
@@ -362,8 +384,10 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
     const bool contiguous = v >= chunk_log2;
     const size_t need = static_cast<size_t>(nbuf) * C * sizeof(double2) * (contiguous ? 1 : 2);
     if (ctx->stage_bytes < need) {
-        cudaStreamSynchronize(ctx->comm_stream);
-        cudaStreamSynchronize(ctx->copy_stream);
+        if (int rc = wait_stream(ctx, ctx->comm_stream, "qsv_swap: staging resize"); rc != QSV_OK)
+            return rc;
+        if (int rc = wait_stream(ctx, ctx->copy_stream, "qsv_swap: staging resize"); rc != QSV_OK)
+            return rc;
         if (ctx->d_stage)
             cudaFree(ctx->d_stage);
         ctx->d_stage = nullptr;

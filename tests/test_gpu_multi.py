@@ -130,3 +130,19 @@ def test_two_gpu_swap_paths(two, spec, mode, monkeypatch):
     c = pkg.Circuit.generate(spec)
     got, rep = run_dist(c, 1, 12, 2)
     assert np.abs(got - O.run_local(c)).max() <= 1e-10
+
+
+@pytest.mark.timeout(600)
+def test_rank_failure_aborts_all_ranks(two, monkeypatch):
+    """a rank that fails after the communicator exists aborts the others (ncclCommAbort
+    from the failing thread) — the call raises with every rank's diagnostics instead of hanging
+    in the first swap's collectives."""
+    monkeypatch.setenv("QSV_INJECT_FAIL_RANK", "1")
+    c = pkg.Circuit.generate("random:20:10:2")
+    with pytest.raises(RuntimeError) as ei:
+        run_dist(c, 1, 12, 2)
+    msg = str(ei.value)
+    assert "rank 1" in msg and "injected" in msg
+    monkeypatch.delenv("QSV_INJECT_FAIL_RANK")
+    got, _ = run_dist(c, 1, 12, 2)  # the library is usable again afterwards
+    assert np.abs(got - O.run_local(c)).max() <= 1e-10
