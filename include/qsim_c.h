@@ -91,7 +91,10 @@ void qsim_circuit_free(qsim_circuit* c);
 int qsim_circuit_parse_qasm(const char* text, int64_t len, qsim_circuit** out, int* line, int* col);
 int qsim_circuit_emit_qasm(const qsim_circuit* c, int matrix_export, char* buf, int64_t cap, int64_t* needed);
 /* Exports the device program of the plan (include/qsv.h structures).  Call
- * with NULL arrays to get the counts, then again with buffers of that size. */
+ * with NULL arrays to get the counts, then again with buffers of that size:
+ * on input the counts are the capacities of the non-NULL arrays; the plan is
+ * rebuilt, and if it no longer fits (its options read the environment) the call
+ * writes the needed sizes back and returns QSV_E_ARG without copying. */
 int qsim_plan_export(const qsim_circuit* c, const qsim_plan_opts* opts, int n_local, int* nsteps, int* nops,
                      int* nprims, int64_t* pool_len, void* steps, void* ops, void* prims, double* pool);
 

@@ -316,10 +316,16 @@ int qsim_plan_export(const qsim_circuit* c, const qsim_plan_opts* opts, int n_lo
         qsim::PlanOptions o = to_opts(opts);
         o.n_local = n_local;
         const qsim::Plan p = qsim::make_plan(c->c, o);
+        // in: capacities of the non-null arrays; out: the sizes the plan needs
+        const bool fits = (!steps || static_cast<size_t>(std::max(*nsteps, 0)) >= p.steps.size()) &&
+                          (!ops || static_cast<size_t>(std::max(*nops, 0)) >= p.ops.size()) &&
+                          (!prims || static_cast<size_t>(std::max(*nprims, 0)) >= p.prims.size()) &&
+                          (!pool || static_cast<size_t>(std::max<int64_t>(*pool_len, 0)) >= p.pool.size() / 2);
         *nsteps = static_cast<int>(p.steps.size());
         *nops = static_cast<int>(p.ops.size());
         *nprims = static_cast<int>(p.prims.size());
         *pool_len = static_cast<int64_t>(p.pool.size() / 2);
+        REQUIRE(fits, "qsim_plan_export: a buffer is smaller than the plan (the needed sizes were written back)");
         if (steps)
             std::memcpy(steps, p.steps.data(), p.steps.size() * sizeof(qsv_step_desc));
         if (ops)

@@ -1352,21 +1352,22 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
                                 }
                         }
                     }
+                    // victim order: farthest next local use (Belady), then fewest remaining
+                    // uses, then the highest slot — compared as a tuple, not a packed score
                     int best = -1;
                     for (int relax = 0; relax < 2 && best < 0; ++relax) {
-                        long long best_score = std::numeric_limits<long long>::max();
+                        auto key = [&](int l) {
+                            return std::make_tuple(-static_cast<long long>(next_need[l]),
+                                                   static_cast<long long>(remaining[l]), -pk.pos[l]);
+                        };
                         for (int l = 0; l < c.n; ++l) {
                             const int p = pk.pos[l];
                             if (p >= plan.n_local || contains(need, l))
                                 continue;
                             if (relax == 0 && (p < pk.Lmin || contains(pk.targets, p)))
                                 continue;
-                            const long long score = -next_need[l] * (1LL << 20) +
-                                                    static_cast<long long>(remaining[l]) * 64 - p;
-                            if (score < best_score) {
-                                best_score = score;
+                            if (best < 0 || key(l) < key(best))
                                 best = l;
-                            }
                         }
                     }
                     if (best < 0)

@@ -74,3 +74,23 @@ def test_program_validate_rejects_bad_programs():
     st.nhigh = 1
     op.mat_off = 3  # matrix outside the pool
     assert L.qsv_program_validate(16, 16, 0, C.byref(st), 1, C.byref(op), 1, None, 0, pool, C.c_size_t(4)) == -1
+
+
+def test_plan_export_capacity_checked():
+    """the second qsim_plan_export call checks the caller's capacities."""
+    import ctypes as C
+    import paper_2509_04955_b200 as pkg
+    from tests import dist_emulator as E
+    c = pkg.Circuit.generate("random:12:6:2")
+    L = pkg.load_qsim()
+    o = pkg.PlanOptions().to_c()
+    ns, no, npr, pl = C.c_int(), C.c_int(), C.c_int(), C.c_int64()
+    assert L.qsim_plan_export(c._h, C.byref(o), 12, C.byref(ns), C.byref(no), C.byref(npr), C.byref(pl),
+                              None, None, None, None) == 0
+    need = no.value
+    assert need >= 2
+    ops = (E.Op * need)()
+    no.value = need - 1  # too small
+    rc = L.qsim_plan_export(c._h, C.byref(o), 12, C.byref(ns), C.byref(no), C.byref(npr), C.byref(pl),
+                            None, ops, None, None)
+    assert rc != 0 and no.value == need
