@@ -372,6 +372,60 @@ def emit_json(line):
     print(json.dumps(line), flush=True)
 
 
+EXTRA_CONFIGS = [
+    # (label, spec, PlanOptions overrides): BASELINE.json configs[0], [1] contraction off, [2], [3]
+    ("qft24", "qft:24", {}),
+    ("random30_fusion_off", "random:30:20:2", {"fusion": False}),
+    ("uccsd28", "uccsd:28:100000:3", {}),
+    ("hea33", "hea:33:5:4", {}),
+]
+
+
+def measure_config(pkg, spec, overrides, steps, hbm_peak, f64_peak, device=0) -> dict:
+    """One BASELINE.json config on one GPU: plan + JIT (untimed), 1 warm-up run, then `steps`
+    timed runs from |0...0> (CUDA events on the engine stream, clocks sampled), plus the
+    per-pass profile for the roofline fraction.  The engine is freed before returning."""
+    opts = pkg.PlanOptions()
+    for k, v in overrides.items():
+        setattr(opts, k, v)
+    circ = pkg.Circuit.generate(spec)
+    t0 = time.perf_counter()
+    eng = pkg.Engine(circ, opts, device=device)
+    setup_s = time.perf_counter() - t0
+    jit = eng.jit_info()
+    st = eng.stats
+    info = eng.steps()
+    eng.set_basis(0)
+    eng.run()
+    eng.sync()
+    clocks = ClockSampler(device)
+    clocks.start()
+    ms = eng.time(steps, basis=0) / steps
+    clk = clocks.stop()
+    eng.set_basis(0)
+    prof = eng.profile()
+    norm = eng.norm_sq()
+    eng.close()
+    pass_ms = [p for p, s in zip(prof, info) if s["kind"] == "pass"]
+    pbytes = [s["hbm_bytes"] for s in info if s["kind"] == "pass"]
+    pflops = [s["flops"] for s in info if s["kind"] == "pass"]
+    t_roof = sum(max(b / (hbm_peak * 1e9), f / (f64_peak * 1e12)) for b, f in zip(pbytes, pflops))
+    per_pass_frac = [max(b / (hbm_peak * 1e9), f / (f64_peak * 1e12)) / (t / 1e3)
+                     for b, f, t in zip(pbytes, pflops, pass_ms) if t > 0]
+    return {
+        "workload": spec, "options": overrides or "default", "gates": st["gates_in"], "passes": st["passes"],
+        "circuit_time_s": ms / 1e3, "gates_per_s": st["gates_in"] / (ms / 1e3), "timed_runs": steps,
+        "hbm_gbs_avg": (sum(pbytes) / 1e9) / (sum(pass_ms) / 1e3) if pass_ms else None,
+        "hbm_floor_s": sum(pbytes) / (hbm_peak * 1e9),
+        "roofline_time_s": t_roof, "roofline_frac": t_roof / (ms / 1e3),
+        "passes_at_or_above_0.70": sum(1 for f in per_pass_frac if f >= 0.70),
+        "min_pass_frac": min(per_pass_frac) if per_pass_frac else None,
+        "achieved_tflops": sum(pflops) / (sum(pass_ms) / 1e3) / 1e12 if pass_ms else None,
+        "norm_error": abs(norm - 1.0), "jit_kernels": jit["kernels"], "setup_s": round(setup_s, 2),
+        "clocks": clk,
+    }
+
+
 def main():
     quiet_stdout()
     ap = argparse.ArgumentParser()
@@ -387,6 +441,8 @@ def main():
                     help="tile-qubit relabelling: 0 off, 1 auto (kept when it saves passes), 2 always")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true",
+                    help="skip the other BASELINE.json configs (QFT-24, random-30 DAGC off, UCCSD-28, HEA-33)")
     ap.add_argument("--e2e-sequential", action="store_true", help="one engine, no copy/compute overlap")
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per reference step")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds for the cpu_baseline sample")
@@ -516,6 +572,16 @@ def main():
         cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "gbs", "per_class", "cpu_model",
                                    "nproc", "oracle_build")}
 
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra_configs:
+        eng.close()  # HEA-33 needs 128 GiB of the GPU
+        extra = {}
+        for label, spec, ov in EXTRA_CONFIGS:
+            try:
+                extra[label] = measure_config(pkg, spec, ov, 2, hbm_peak, f64_peak)
+            except Exception as ex:  # reported, never silently dropped
+                extra[label] = {"workload": spec, "error": str(ex)[:300]}
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -561,6 +627,7 @@ def main():
         "norm_error": abs(norm - 1.0) if world == 1 else None,
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "configs": extra,
         "gpu_launches": launches,
         "clocks": clk,
         "wall_s_timed_region": wall,
