@@ -145,20 +145,41 @@ std::string u64(uint64_t x) {
 }
 
 // Body of one pass (ops applied to one tile) as source text.
-std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
+// Tile groups per CTA of a specialised pass kernel (pass_pipeline MT): 3 lockstep
+// groups of 128 threads for 11-qubit tiles (QSV_JIT_MT overrides, 1 = one tile per CTA).
+int jit_mt(int K) {
+    const int mt = env_int("QSV_JIT_MT", 3, 1, 3);
+    return (K == 11 && !split_blocks()) ? mt : 1;
+}
+
+// `mt` > 1: the CTA barrier of an op whose application depends on the tile (out-of-tile
+// controls) is hoisted out of the condition so every tile group meets it; ops with
+// internal CTA barriers under such a condition make the pass unsuitable (mt_ok = false).
+std::string gen_ops(const Step& s, const unsigned char* blob, int& minb, int mt = 1, bool* mt_ok = nullptr) {
     const int K = s.geom.K;
     const int NT = threads_for_k(K);
     const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
     std::ostringstream o;
     minb = K >= 12 ? 1 : 3;
+    if (mt_ok)
+        *mt_ok = true;
     for (int i = 0; i < s.nops; ++i) {
         const TileOp& op = ops[i];
         const std::string opref = "*reinterpret_cast<const qsv::TileOp*>(blob + " +
                                   std::to_string(i * sizeof(TileOp)) + ")";
         o << "  {\n";
-        if (op.xctrl)
+        if (op.xctrl && mt > 1) {
+            if (op.kind == QSV_OP_RELABEL || (op.kind == QSV_OP_DENSE && op.k == 5)) {
+                if (mt_ok)
+                    *mt_ok = false;
+            }
+            o << "  __syncthreads();\n";
             o << "  if ((full_base & " << u64(op.xctrl) << ") == " << u64(op.xctrl) << ") {\n";
-        o << "  __syncthreads();\n";
+        } else {
+            if (op.xctrl)
+                o << "  if ((full_base & " << u64(op.xctrl) << ") == " << u64(op.xctrl) << ") {\n";
+            o << "  __syncthreads();\n";
+        }
         switch (op.kind) {
         case QSV_OP_DENSE:
             if (op.k == 5) {
@@ -394,7 +415,7 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
             }
             o << "  qsv::jit_rblock<" << K << ", " << NT << ", " << KB << ", " << u32(op.fmask) << ", "
               << u32(op.tctrl) << ", " << u32(m[0]) << ", " << u32(m[1]) << ", " << u32(m[2]) << ", " << u32(m[3])
-              << ", " << u32(op.rot_tab) << (fold ? ", true" : "") << ">(tile, [&](double2 (&v)[" << NV << "], uint32_t r) {\n";
+              << ", " << u32(op.rot_tab) << (fold ? ", true" : "") << ">(tile, [&](double2 (&v)[" << NV << "], uint32_t& r) {\n";
             if (last > i) {
                 // hoisted constants must precede the call: re-emit the call after them
                 std::string call = o.str();
@@ -405,10 +426,24 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
             }
             o << "    (void)r;\n";
             const DevPrim* pr = reinterpret_cast<const DevPrim*>(blob + op.prim_byte);
+            // Member rotation tracked through the body: register j holds member j ^ r.  A CX
+            // whose control may be rotated swaps the pairs with register bit C = 1 (pure
+            // renaming) and, on lanes whose rotation has bit C set, flips rotation bit T
+            // instead of moving data (the complement set of pairs = all pairs composed with
+            // these).  `rot` is the set of bits of r that may be non-zero at this point; the
+            // host stores every U1/U2 matrix in all rotation variants.
+            uint32_t rot = rot_any;
+            const bool dyn_rot = env_int("QSV_JIT_DYNROT", 1, 0, 1) != 0;
             for (int p = 0; p < op.nprim; ++p) {
                 const DevPrim& q = pr[p];
                 const std::string mat = "reinterpret_cast<const double2*>(blob + " + std::to_string(q.data_byte) + ")";
-                const bool ra = (rot_any >> q.a) & 1u, rb = (rot_any >> q.b) & 1u;
+                const bool ra = (rot >> q.a) & 1u, rb = (rot >> q.b) & 1u;
+                if (q.kind == QSV_PRIM_CX && ra && dyn_rot) {
+                    o << "    qsv::rb_cx_plain<" << NV << ", " << int(q.a) << ", " << int(q.b) << ">(v);\n";
+                    o << "    r ^= ((r >> " << int(q.a) << ") & 1u) << " << int(q.b) << ";\n";
+                    rot |= 1u << q.b;
+                    continue;
+                }
                 switch (q.kind) {
                 case QSV_PRIM_U1:
                 case QSV_PRIM_U1R:
@@ -433,7 +468,7 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb) {
                         o << "    qsv::rb_cx_plain<" << NV << ", " << int(q.a) << ", " << int(q.b) << ">(v);\n";
                     break;
                 default:
-                    o << "    qsv::rb_diag<" << NV << ">(v, " << mat << ", " << (rot_any ? "r" : "0u") << ");\n";
+                    o << "    qsv::rb_diag<" << NV << ">(v, " << mat << ", " << (rot ? "r" : "0u") << ");\n";
                     break;
                 }
             }
@@ -475,14 +510,15 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 int tile_nbuf() { return env_int("QSV_TILE_NBUF", kNumBuf, 2, 4); }
 int tile_pd() { return env_int("QSV_TILE_PD", tile_nbuf() - 1, 1, tile_nbuf() - 1); }
 
-std::string kernel_source(const std::string& name, int K, int minb, const std::string& body) {
+std::string kernel_source(const std::string& name, int K, int minb, const std::string& body, int mt = 1) {
     std::ostringstream o;
     const int NT = threads_for_k(K);
-    o << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << minb << ") " << name
+    o << "extern \"C\" __global__ void __launch_bounds__(" << NT * mt << ", " << (mt > 1 ? 1 : minb) << ") " << name
       << "(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, uint32_t blob_bytes,\n"
       << "    const __grid_constant__ qsv::GeomArg geom, uint64_t rank_base, uint64_t ntiles) {\n"
       << "  qsv::pass_pipeline<" << K << ", " << NT << ", " << tile_nbuf() << ", " << tile_pd() << ", "
-      << (env_int("QSV_TMA_SPREAD", 1, 0, 1) ? "true" : "false") << ">(psi, gblob, blob_bytes, geom, rank_base, ntiles,\n"
+      << (env_int("QSV_TMA_SPREAD", 1, 0, 1) ? "true" : "false") << ", " << mt
+      << ">(psi, gblob, blob_bytes, geom, rank_base, ntiles,\n"
       << "    [&](double2* tile, const unsigned char* blob, uint64_t full_base) {\n"
       << "  (void)full_base;\n"
       << body << "  });\n}\n";
@@ -609,9 +645,13 @@ namespace {
 // Distinct pass structures of a program -> kernel sources (host only).
 struct JitPlan {
     std::vector<std::string> bodies;
-    std::vector<int> kernel_k, kernel_minb;
+    std::vector<int> kernel_k, kernel_minb, kernel_mt;
     std::vector<int> jit_of_step;
 };
+
+// Dynamic SMEM of a specialised kernel: MT groups x NBUF tile buffers + the pass blob.
+size_t jit_tile_smem(int K, int mt) { return sizeof(double2) * static_cast<size_t>(mt) * tile_nbuf() * (size_t{1} << K); }
+constexpr size_t kSmemPerCta = 227 * 1024 - 4096;  // opt-in limit minus the static arrays
 
 JitPlan plan_kernels(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels) {
     JitPlan jp;
@@ -622,8 +662,15 @@ JitPlan plan_kernels(const std::vector<Step>& steps, const unsigned char* host_b
         if (s.desc.kind != QSV_STEP_PASS || s.geom.K < 4)
             continue;
         int minb = 3;
-        const std::string body = gen_ops(s, host_blobs + s.blob_off, minb);
-        const std::string key = std::to_string(s.geom.K) + "|" + std::to_string(minb) + "|" + body;
+        int mt = jit_mt(s.geom.K);
+        bool mt_ok = true;
+        std::string body = gen_ops(s, host_blobs + s.blob_off, minb, mt, &mt_ok);
+        if (mt > 1 && (!mt_ok || jit_tile_smem(s.geom.K, mt) + s.blob_bytes > kSmemPerCta)) {
+            mt = 1;
+            body = gen_ops(s, host_blobs + s.blob_off, minb, 1, nullptr);
+        }
+        const std::string key = std::to_string(s.geom.K) + "|" + std::to_string(minb) + "|" + std::to_string(mt) +
+                                "|" + body;
         auto it = uniq.find(key);
         if (it == uniq.end()) {
             if (static_cast<int>(jp.bodies.size()) >= max_kernels)
@@ -632,6 +679,7 @@ JitPlan plan_kernels(const std::vector<Step>& steps, const unsigned char* host_b
             jp.bodies.push_back(body);
             jp.kernel_k.push_back(s.geom.K);
             jp.kernel_minb.push_back(minb);
+            jp.kernel_mt.push_back(mt);
         }
         jp.jit_of_step[i] = it->second;
     }
@@ -650,7 +698,8 @@ bool compile_kernels(const JitPlan& jp, std::vector<std::vector<char>>& cubins, 
     for (int u = 0; u < nunits; ++u) {
         std::string src = kDeviceSource;
         for (int k = u * kKernelsPerUnit; k < std::min(nk, (u + 1) * kKernelsPerUnit); ++k)
-            src += kernel_source("qsv_jit_" + std::to_string(k), jp.kernel_k[k], jp.kernel_minb[k], jp.bodies[k]);
+            src += kernel_source("qsv_jit_" + std::to_string(k), jp.kernel_k[k], jp.kernel_minb[k], jp.bodies[k],
+                                 jp.kernel_mt[k]);
         srcs[u] = std::move(src);
     }
     cubins.assign(nunits, {});
@@ -746,11 +795,13 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
                 return QSV_E_CUDA;
             }
             const int K = kernel_k[k];
-            const size_t tile_smem = sizeof(double2) * tile_nbuf() * (size_t{1} << K);
+            const int mt = jp.kernel_mt[k];
+            const size_t tile_smem = jit_tile_smem(K, mt);
             d.set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
-                       static_cast<int>(tile_smem + kMaxBlobBytes));
+                       static_cast<int>(std::min(tile_smem + kMaxBlobBytes, kSmemPerCta)));
             prog->jit_kernels[k].func = f;
-            prog->jit_kernels[k].nt = threads_for_k(K);
+            prog->jit_kernels[k].nt = threads_for_k(K) * mt;
+            prog->jit_kernels[k].mt = mt;
             prog->jit_kernels[k].tile_smem = tile_smem;
         }
     }
@@ -783,7 +834,8 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
     if (tiles == 0)
         return cudaSuccess;
     const int sms = rg.sms > 0 ? std::min(rg.sms, st->ctx->sm_count) : st->ctx->sm_count;
-    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * sms);
+    const uint64_t ctas_needed = (tiles + jk.mt - 1) / jk.mt;
+    const uint64_t grid = std::min<uint64_t>(ctas_needed, static_cast<uint64_t>(per_sm) * sms);
     double2* psi = st->amps;
     uint32_t bb = s.blob_bytes;
     uint64_t rb = rank_base, nt = tiles;

@@ -7,6 +7,14 @@
 
 namespace qsv {
 
+// Thread index within the tile's thread group: a multi-tile CTA (pass_pipeline MT > 1)
+// runs MT groups of NT threads, each on its own tile, in lockstep (the per-op CTA
+// barriers keep every group at the same point of the straight-line pass code, so
+// the warps a scheduler interleaves fetch the same instructions).  Every op body is
+// written for one group of NT threads (NT is a power of two and a template
+// parameter wherever this is used).
+#define QSV_LTID (threadIdx.x & static_cast<unsigned>(NT - 1))
+
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -122,8 +130,8 @@ __device__ __forceinline__ void dense_op(double2* tile, const TileOp& op, const 
     constexpr int CPL = D / S;            // columns per lane
     constexpr int NW = NT / 32;
     constexpr uint32_t PER_STEP = NW * GPW;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    const int lane = QSV_LTID & 31;
+    const int warp = QSV_LTID >> 5;
     const int sub = lane / LPG;
     const int r = (lane % LPG) / S;
     const int sp = (lane % LPG) % S;
@@ -185,7 +193,7 @@ __device__ __forceinline__ void relabel_op(double2* __restrict__ tile, const Til
         uint32_t sb = 0, db = 0;
 #pragma unroll
         for (int b = 0; b < TB; ++b)
-            if ((threadIdx.x >> b) & 1u) {
+            if ((QSV_LTID >> b) & 1u) {
                 sb ^= col[b];
                 db ^= col[16 + b];
             }
@@ -216,11 +224,11 @@ __device__ __forceinline__ void relabel_op(double2* __restrict__ tile, const Til
             tile[x] = v[j];
         }
     } else {
-        const bool on = threadIdx.x < TILE;
+        const bool on = QSV_LTID < TILE;
         uint32_t sb = 0, db = 0;
 #pragma unroll
         for (int b = 0; b < K; ++b)
-            if ((threadIdx.x >> b) & 1u) {
+            if ((QSV_LTID >> b) & 1u) {
                 sb ^= col[b];
                 db ^= col[16 + b];
             }
@@ -240,9 +248,9 @@ __device__ __forceinline__ void xperm_op(double2* tile, const TileOp& op) {
     const uint32_t F = op.fmask;
     const uint32_t groups = 1u << (K - nfix);
     const uint32_t tb = 1u << op.tpos[0];
-    if (threadIdx.x >= groups)
+    if (QSV_LTID >= groups)
         return;
-    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    uint32_t b = deposit(QSV_LTID, op.fixpos, nfix);
     const uint32_t dstep = deposit(NT, op.fixpos, nfix);
     const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
 #pragma unroll 2
@@ -269,9 +277,9 @@ __device__ __forceinline__ void diag_op(double2* tile, const TileOp& op, const u
     uint32_t e0 = 0;
     for (int j = nin; j < k; ++j)
         e0 |= static_cast<uint32_t>((full_base >> op.xbit[j - nin]) & 1ull) << j;
-    if (threadIdx.x >= groups)
+    if (QSV_LTID >= groups)
         return;
-    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    uint32_t b = deposit(QSV_LTID, op.fixpos, nfix);
     const uint32_t dstep = deposit(NT, op.fixpos, nfix);
     const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
     if (nin == 0) {
@@ -318,7 +326,7 @@ __device__ __forceinline__ void dense5_op(double2* tile, const TileOp& op, const
     const int rows = D / R;
 #pragma unroll 1
     for (uint32_t base_t = 0; base_t < (many ? groups : 1u); base_t += NT) {
-        const int t = static_cast<int>(threadIdx.x);
+        const int t = static_cast<int>(QSV_LTID);
         const uint32_t g = many ? base_t + t : static_cast<uint32_t>(t) % groups;
         const int rb = many ? 0 : t / static_cast<int>(groups);
         const bool act = many ? g < groups : t < static_cast<int>(groups) * R;
@@ -508,15 +516,15 @@ __device__ __forceinline__ void rblock_op(double2* tile, const TileOp& op, const
     const uint32_t tctrl = op.tctrl;
     const uint32_t F = op.fmask;
     const uint32_t groups = 1u << (K - nfix);
-    if (threadIdx.x >= groups)
+    if (QSV_LTID >= groups)
         return;
     // this lane's member rotation (bank spreading), as block bits and tile offset
-    const uint32_t r = (op.rot_tab >> (4 * (threadIdx.x & 7))) & 15u;
+    const uint32_t r = (op.rot_tab >> (4 * (QSV_LTID & 7))) & 15u;
     uint32_t offr = 0;
 #pragma unroll
     for (int i = 0; i < KB; ++i)
         offr |= ((r >> i) & 1u) ? mk[i] : 0u;
-    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    uint32_t b = deposit(QSV_LTID, op.fixpos, nfix);
     const uint32_t dstep = deposit(NT, op.fixpos, nfix);
     const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
     const DevPrim* prims = reinterpret_cast<const DevPrim*>(blob + op.prim_byte);
@@ -564,9 +572,9 @@ __device__ __forceinline__ void parphase_op(double2* tile, const TileOp& op, con
     const uint32_t tctrl = op.tctrl;
     const uint32_t F = op.fmask;
     const uint32_t groups = 1u << (K - nfix);
-    if (threadIdx.x >= groups)
+    if (QSV_LTID >= groups)
         return;
-    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    uint32_t b = deposit(QSV_LTID, op.fixpos, nfix);
     const uint32_t dstep = deposit(NT, op.fixpos, nfix);
     const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
 #pragma unroll 4
@@ -625,9 +633,9 @@ __device__ __forceinline__ void phaseprod_op(double2* tile, const TileOp& op, co
     const uint32_t tctrl = op.tctrl;
     const uint32_t F = op.fmask;
     const uint32_t groups = 1u << (K - nfix);
-    if (threadIdx.x >= groups)
+    if (QSV_LTID >= groups)
         return;
-    uint32_t b = deposit(threadIdx.x, op.fixpos, nfix);
+    uint32_t b = deposit(QSV_LTID, op.fixpos, nfix);
     const uint32_t dstep = deposit(NT, op.fixpos, nfix);
     const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
 #pragma unroll 4
@@ -665,17 +673,24 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const GeomArg& g) {
 // warp j % NW) and arms the mbarrier for those bytes (one arrival per warp), instead of
 // warp 0 carrying all of it; each lane only ever waits for its own store groups, which
 // read exactly the SMEM runs it reloads.  Warps then reach the per-op barriers together.
-template <int K, int NT, int NBUF = kNumBuf, int PD = NBUF - 1, bool SPREAD = true, typename Ops>
+template <int K, int NT, int NBUF = kNumBuf, int PD = NBUF - 1, bool SPREAD = true, int MT = 1, typename Ops>
 __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const unsigned char* __restrict__ gblob,
                                               uint32_t blob_bytes, const GeomArg& geom, uint64_t rank_base,
                                               uint64_t ntiles, Ops&& ops) {
+    // MT tile groups of NT threads per CTA (see QSV_LTID): group `sub` owns NBUF buffers
+    // and mbarriers and processes tiles T * MT + sub of the CTA's tile sequence T.  All
+    // groups run the same number of iterations (a group past the last tile still runs
+    // the ops on its stale buffer, for the shared barriers, but neither loads nor stores).
     constexpr int TILE = 1 << K;
     extern __shared__ __align__(128) unsigned char smem[];
-    double2* bufs = reinterpret_cast<double2*>(smem);
     static_assert(PD >= 1 && PD < NBUF, "prefetch distance must be in [1, NBUF)");
-    unsigned char* blob = smem + sizeof(double2) * NBUF * TILE;
+    static_assert(MT >= 1 && MT <= 4, "tile groups per CTA must be in [1, 4]");
+    const int sub = MT > 1 ? static_cast<int>(threadIdx.x) / NT : 0;
+    double2* bufs = reinterpret_cast<double2*>(smem) + static_cast<size_t>(sub) * NBUF * TILE;
+    unsigned char* blob = smem + sizeof(double2) * MT * NBUF * TILE;
     __shared__ uint64_t hi_off[1 << QSV_MAX_HIGH];
-    __shared__ __align__(8) uint64_t mbar[NBUF];
+    __shared__ __align__(8) uint64_t mbar_all[MT * NBUF];
+    uint64_t* mbar = mbar_all + sub * NBUF;
 
     const int nh = 1 << geom.nhigh;
     const int L = geom.L;
@@ -687,7 +702,7 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     const int RL = L + m;
     const int nruns = nh >> m;
     const uint32_t run_bytes = static_cast<uint32_t>(sizeof(double2)) << RL;
-    for (int j = threadIdx.x; j < nh; j += NT) {
+    for (int j = threadIdx.x; j < nh; j += NT * MT) {
         uint64_t o = 0;
         for (int i = 0; i < geom.nhigh; ++i)
             o |= static_cast<uint64_t>((j >> i) & 1) << geom.high[i];
@@ -696,13 +711,13 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     {
         const int4* src = reinterpret_cast<const int4*>(gblob);
         int4* dst = reinterpret_cast<int4*>(blob);
-        for (uint32_t i = threadIdx.x; i < blob_bytes / 16; i += NT)
+        for (uint32_t i = threadIdx.x; i < blob_bytes / 16; i += NT * MT)
             dst[i] = __ldg(src + i);
     }
-    constexpr int NW = SPREAD ? NT / 32 : 1;  // warps issuing TMA copies
+    constexpr int NW = SPREAD ? NT / 32 : 1;  // warps of a group issuing TMA copies
     if (threadIdx.x == 0) {
-        for (int b = 0; b < NBUF; ++b)
-            mbar_init(&mbar[b], NW);
+        for (int b = 0; b < MT * NBUF; ++b)
+            mbar_init(&mbar_all[b], NW);
         fence_mbar_init();
     }
     __syncthreads();
@@ -711,9 +726,10 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     // The issuing warps drive the TMA bulk engine: lane 0 of each arms the tile's
     // mbarrier with its byte count, then its lanes issue that warp's run copies.
     const int lane = threadIdx.x & 31;
-    const int warp = static_cast<int>(threadIdx.x >> 5);
+    const int warp = static_cast<int>(QSV_LTID >> 5);
     const bool issuer = warp < NW;
     const int my_runs = nruns > warp ? (nruns - warp + NW - 1) / NW : 0;
+    auto tile_of = [&](uint64_t T) { return T * MT + static_cast<uint64_t>(sub); };
     auto issue_load = [&](uint64_t t, int b) {
         const uint64_t base = tile_base(geom.tile0 + t, geom);
         double2* dst = bufs + b * TILE;
@@ -726,20 +742,24 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         }
     };
 
+    const uint64_t nT = (ntiles + MT - 1) / MT;  // CTA-level tile steps
     if (issuer) {
         for (int s = 0; s < PD; ++s) {
-            const uint64_t t = blockIdx.x + s * stride;
-            if (t < ntiles)
+            const uint64_t t = tile_of(blockIdx.x + s * stride);
+            if (blockIdx.x + s * stride < nT && t < ntiles)
                 issue_load(t, s);
         }
     }
 
     int it = 0;
-    for (uint64_t t = blockIdx.x; t < ntiles; t += stride, ++it) {
+    for (uint64_t T = blockIdx.x; T < nT; T += stride, ++it) {
         const int b = it % NBUF;
+        const uint64_t t = tile_of(T);
+        const bool valid = t < ntiles;
         if (issuer) {
-            const uint64_t tn = t + PD * stride;
-            if (tn < ntiles) {
+            const uint64_t Tn = T + PD * stride;
+            const uint64_t tn = tile_of(Tn);
+            if (Tn < nT && tn < ntiles) {
                 // Buffer (it + PD) % NBUF was last stored from in iteration
                 // it + PD - NBUF: every lane waits for its own store groups that old.
                 bulk_wait_read<NBUF - PD - 1>();
@@ -747,17 +767,20 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
                 issue_load(tn, (it + PD) % NBUF);
             }
         }
-        mbar_wait(&mbar[b], static_cast<uint32_t>((it / NBUF) & 1));
+        if (valid)
+            mbar_wait(&mbar[b], static_cast<uint32_t>((it / NBUF) & 1));
         double2* tile = bufs + b * TILE;
-        const uint64_t base = tile_base(geom.tile0 + t, geom);
+        const uint64_t base = valid ? tile_base(geom.tile0 + t, geom) : 0;
         const uint64_t full_base = rank_base | base;
+        if (MT > 1 && !valid && issuer)
+            bulk_wait_read_all();  // the stale buffer may still feed a store; every op starts with a CTA barrier
 
         ops(tile, blob, full_base);
         // Make this thread's generic-proxy SMEM writes visible to the bulk-copy
-        // (async) proxy, then let thread 0 stream the tile back.
+        // (async) proxy, then let the issuing warps stream the tile back.
         fence_proxy_async();
         __syncthreads();
-        if (issuer) {
+        if (issuer && valid) {
             for (int k = lane; k < my_runs; k += 32) {
                 const int j = warp + NW * k;
                 bulk_store(psi + base + hi_off[j << m], tile + (j << RL), run_bytes);
@@ -878,9 +901,9 @@ template <int K, int NT, uint32_t F, uint32_t TCTRL, uint32_t M0, uint32_t M1, u
 __device__ __forceinline__ void jit_rblock_split(double2* tile, Body&& body, Epi&& epi) {
     static_assert((1 << (K - cpopc(F))) * 2 == NT, "split blocks need exactly two threads per group");
     constexpr uint32_t M[4] = {M0, M1, M2, M3};
-    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t lane = QSV_LTID & 31u;
     const uint32_t h = lane >> 4;
-    const uint32_t g = ((threadIdx.x >> 5) << 4) | (lane & 15u);
+    const uint32_t g = ((QSV_LTID >> 5) << 4) | (lane & 15u);
     const uint32_t r = ROT ? ((ROT >> (4 * (lane & 7))) & 15u) : 0u;
     const uint32_t offr = ((r & 1u) ? M0 : 0u) | ((r & 2u) ? M1 : 0u) | ((r & 4u) ? M2 : 0u) | ((r & 8u) ? M3 : 0u);
     const uint32_t base = cdeposit(g, F) | TCTRL | offr;
@@ -936,19 +959,24 @@ __device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi
     constexpr uint32_t groups = 1u << (K - cpopc(F));
     constexpr uint32_t dstep = cdeposit(NT, F);
     constexpr uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
-    if (groups < static_cast<uint32_t>(NT) && threadIdx.x >= groups)
+    if (groups < static_cast<uint32_t>(NT) && QSV_LTID >= groups)
         return;
-    const uint32_t r = ROT ? ((ROT >> (4 * (threadIdx.x & 7))) & 15u) : 0u;
-    const uint32_t offr = ((r & 1u) ? M0 : 0u) | ((r & 2u) ? M1 : 0u) | ((r & 4u) ? M2 : 0u) | ((r & 8u) ? M3 : 0u);
-    uint32_t b = cdeposit(threadIdx.x, F);
+    const uint32_t r0 = ROT ? ((ROT >> (4 * (QSV_LTID & 7))) & 15u) : 0u;
+    auto rot_off = [](uint32_t rr) {
+        return ((rr & 1u) ? M0 : 0u) | ((rr & 2u) ? M1 : 0u) | ((rr & 4u) ? M2 : 0u) | ((rr & 8u) ? M3 : 0u);
+    };
+    const uint32_t offr = rot_off(r0);
+    uint32_t b = cdeposit(QSV_LTID, F);
 #pragma unroll 1
     for (uint32_t st = 0; st < steps; ++st) {
-        const uint32_t base = b | TCTRL | offr;
+        const uint32_t base_in = b | TCTRL | offr;
         double2 v[NV];
 #pragma unroll
         for (int j = 0; j < NV; ++j)
-            v[j] = tile[base ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))];
-        body(v, r);
+            v[j] = tile[base_in ^ (((j & 1) ? M0 : 0u) | ((j & 2) ? M1 : 0u) | ((j & 4) ? M2 : 0u) | ((j & 8) ? M3 : 0u))];
+        uint32_t r = r0;
+        body(v, r);  // may update the rotation (CX on a rotated control)
+        const uint32_t base = b | TCTRL | rot_off(r);
         epib(v, base);
         if constexpr (PERM) {
             static_assert(groups == static_cast<uint32_t>(NT), "folded relabel needs one group per thread");

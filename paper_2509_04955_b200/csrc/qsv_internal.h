@@ -87,7 +87,8 @@ struct qsv_state {
 namespace qsv {
 struct JitKernel {
     void* func = nullptr;    // CUfunction
-    int nt = 0;
+    int nt = 0;              // threads per CTA (mt tile groups)
+    int mt = 1;
     size_t tile_smem = 0;
 };
 } // namespace qsv
