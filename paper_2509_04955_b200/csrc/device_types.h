@@ -39,6 +39,10 @@ typedef unsigned long long uint64_t;
 // Internal (device-only) op kind: the pass relabel appended after a pass's ops
 // (qsv_step_desc::relabel); never appears in a qsv_op_desc.
 #define QSV_OP_RELABEL 16
+// Internal op kind: a 4-qubit register block whose primitive list is heavy enough is
+// compiled on the host into its dense 16x16 unitary and applied with DMMA (FP64
+// tensor-core mma.m8n8k4) instead of DFMA primitives.
+#define QSV_OP_DMMA16 17
 
 namespace qsv {
 

@@ -145,10 +145,13 @@ std::string u64(uint64_t x) {
 }
 
 // Body of one pass (ops applied to one tile) as source text.
-// Tile groups per CTA of a specialised pass kernel (pass_pipeline MT): 3 lockstep
-// groups of 128 threads for 11-qubit tiles (QSV_JIT_MT overrides, 1 = one tile per CTA).
+// Tile groups per CTA of a specialised pass kernel (pass_pipeline MT).  Default 1: three
+// independent CTAs per SM.  QSV_JIT_MT=3 runs 3 lockstep groups of 128 threads per CTA
+// (one CTA per SM, all warps on the same code): measured slower — random-30 345 vs 278 ms,
+// HEA-30 140 vs 114 ms — because lockstep groups also wait for their loads together,
+// which costs more than the instruction-cache misses it saves (profiles/r02_kernel_ab.md).
 int jit_mt(int K) {
-    const int mt = env_int("QSV_JIT_MT", 3, 1, 3);
+    const int mt = env_int("QSV_JIT_MT", 1, 1, 3);
     return (K == 11 && !split_blocks()) ? mt : 1;
 }
 
@@ -191,6 +194,9 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb, int mt 
             break;
         case QSV_OP_RELABEL:
             o << "  qsv::relabel_op<" << K << ", " << NT << ">(tile, " << opref << ", blob);\n";
+            break;
+        case QSV_OP_DMMA16:
+            o << "  qsv::dmma16_op<" << K << ", " << NT << ">(tile, " << opref << ", blob);\n";
             break;
         case QSV_OP_DIAG:
             o << "  qsv::diag_op<" << K << ", " << NT << ">(tile, " << opref << ", blob, full_base);\n";

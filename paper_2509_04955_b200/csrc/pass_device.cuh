@@ -354,6 +354,99 @@ __device__ __forceinline__ void dense5_op(double2* tile, const TileOp& op, const
     }
 }
 
+// ---------------------------------------------------------------- DMMA16
+// Dense 16x16 complex unitary on 4 tile qubits with the FP64 tensor cores.  The
+// complex mat-vec of every group is one column of a real GEMM
+//     [Yr; Yi] (32 x G) = [[Mr, -Mi], [Mi, Mr]] (32 x 32) . [Xr; Xi] (32 x G)
+// cut into mma.sync.m8n8k4.f64 tiles: 4 row blocks (Re members 0-7, 8-15, Im 0-7,
+// 8-15) x 8 k-steps (Re members 0-3, ..., Im members 12-15) per 8 groups.  A warp
+// owns whole 8-group column blocks, so no CTA barrier is needed inside the op: its
+// lanes read the groups (LDS.128 = the Re and Im rows of one member), the MMAs
+// consume every lane's fragment, then the lanes write the results back (STS.128
+// pairs the Re and Im accumulators of one member).  Per amplitude: 64 DMMA MACs
+// (128 flop, the dense cost) issued as 1/4 instruction instead of ~50 DFMA/DMUL.
+// Fragment layout (PTX m8n8k4 .f64): A[g][t], B[t][g], C[g][2t + i] for lane = 4g + t.
+__device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int K, int NT>
+__device__ __forceinline__ void dmma16_op(double2* tile, const TileOp& op, const unsigned char* blob) {
+    constexpr int NW = NT / 32;
+    const uint32_t lane = QSV_LTID & 31u;
+    const uint32_t warp = QSV_LTID >> 5;
+    const uint32_t g = lane >> 2, t = lane & 3u;
+    const uint32_t groups = 1u << (K - op.nfix);
+    const uint32_t nblk = (groups + 7u) >> 3;  // 8-group column blocks
+    if (warp >= nblk)
+        return;
+    const double2* M = reinterpret_cast<const double2*>(blob + op.mat_byte);
+    // A fragments: M[8 mt + g][4 ks + t] for mt < 2, ks < 4 (Re and Im parts; -Im once)
+    double ar[2][4], ai[2][4], an[2][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+            const double2 m = M[(8 * mt + g) * 16 + 4 * ks + t];
+            ar[mt][ks] = m.x;
+            ai[mt][ks] = m.y;
+            an[mt][ks] = -m.y;
+        }
+    // member offsets: B reads members 4q + t, D writes members 8h + g
+    const uint32_t m0 = 1u << op.tpos[0], m1 = 1u << op.tpos[1], m2 = 1u << op.tpos[2], m3 = 1u << op.tpos[3];
+    auto moff = [&](uint32_t j) {
+        return ((j & 1u) ? m0 : 0u) | ((j & 2u) ? m1 : 0u) | ((j & 4u) ? m2 : 0u) | ((j & 8u) ? m3 : 0u);
+    };
+    uint32_t ob[4], od[2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        ob[q] = moff(4u * q + t);
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        od[h] = moff(8u * h + g);
+    const uint32_t tctrl = op.tctrl;
+#pragma unroll 1
+    for (uint32_t blk = warp; blk < nblk; blk += NW) {
+        const uint32_t gb = blk * 8u + g;  // this lane's B column (group)
+        const bool vb = gb < groups;
+        const uint32_t bb = vb ? (deposit(gb, op.fixpos, op.nfix) | tctrl) : 0u;
+        double xr[4], xi[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 x = vb ? tile[bb | ob[q]] : make_double2(0.0, 0.0);
+            xr[q] = x.x;
+            xi[q] = x.y;
+        }
+        double d[4][2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+            d[mt][0] = d[mt][1] = 0.0;
+        // k-outer so the four row-block accumulations are independent chains
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const double b = ks < 4 ? xr[ks] : xi[ks - 4];
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int r = mt & 1, kk = ks & 3;
+                const double a = mt < 2 ? (ks < 4 ? ar[r][kk] : an[r][kk]) : (ks < 4 ? ai[r][kk] : ar[r][kk]);
+                dmma_m8n8k4(d[mt][0], d[mt][1], a, b);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const uint32_t gd = blk * 8u + 2u * t + static_cast<uint32_t>(i);
+            if (gd < groups) {
+                const uint32_t bd = deposit(gd, op.fixpos, op.nfix) | tctrl;
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    tile[bd | od[h]] = make_double2(d[h][i], d[h + 2][i]);
+            }
+        }
+    }
+}
+
 // ---------------------------------------------------------------- RBLOCK
 // A register block holds one group of NV = 2^KB amplitudes (KB = 3 or 4 block
 // qubits) per thread and applies a list of native gates to it in registers;

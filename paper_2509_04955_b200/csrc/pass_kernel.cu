@@ -72,6 +72,9 @@ pass_kernel(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, 
                 if constexpr (K >= 4 && KMAX >= 4) {
                     if (op.k == 4) rblock_op<K, NT, 4>(tile, op, blob);
                 }
+            } else if (op.kind == QSV_OP_DMMA16) {
+                if constexpr (K >= 4)
+                    dmma16_op<K, NT>(tile, op, blob);
             } else if (op.kind == QSV_OP_PARPHASE) {
                 parphase_op<K, NT>(tile, op, blob, full_base);
             } else if (op.kind == QSV_OP_PHASEPROD) {

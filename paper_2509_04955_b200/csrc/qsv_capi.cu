@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -618,6 +619,16 @@ void relabel_columns(int K, const int32_t* rel, uint16_t* scol, uint16_t* dcol) 
     }
 }
 
+// Minimum DFMA/DMUL count per amplitude of a 4-qubit register block's primitive list
+// for it to run as a dense DMMA16 op (QSV_DMMA_MIN_PIPE; 0 disables the tensor path).
+int dmma_min_pipe_ops() {
+    static const int v = [] {
+        const char* e = std::getenv("QSV_DMMA_MIN_PIPE");
+        return e ? std::atoi(e) : 40;
+    }();
+    return v;
+}
+
 int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                  const qsv_op_desc* ops, int nops, const qsv_prim_desc* prims, int nprims,
                  const double* pool, size_t pool_len, qsv::Step& step,
@@ -727,6 +738,8 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                 flops += 8.0 * D * amps * frac;
             }
         } else if (od.kind == QSV_OP_RBLOCK) {
+            double prim_flops = 0.0;
+            int pipe_ops = 0;  // DFMA/DMUL per amplitude of the primitive list
             QSV_REQUIRE(od.k == 3 || od.k == 4, "op: RBLOCK needs 3 or 4 block qubits");
             QSV_REQUIRE(od.prim_begin >= 0 && od.nprim >= 1 && od.prim_begin + od.nprim <= nprims,
                         "op: RBLOCK primitive range outside the primitive array");
@@ -804,9 +817,66 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
                 pl.pdata.push_back(std::move(d));
                 pl.dprims.push_back(dp);
                 flops += fl * amps * frac;
+                prim_flops += fl * amps * frac;
+                pipe_ops += pd.kind == QSV_PRIM_U1 ? 8 : pd.kind == QSV_PRIM_U2 ? 16 : pd.kind == QSV_PRIM_CX ? 0 : 4;
             }
             t.nprim = od.nprim;
             step.geom.kmax = std::max(step.geom.kmax, KB == 4 ? 4 : 1);
+            // Heavy 4-qubit blocks go to the FP64 tensor cores: the block's dense 16x16 unitary
+            // (the primitive product, formed here in double) costs 64 DMMA MACs per amplitude
+            // in ~1/4 instruction, against `pipe_ops` DFMA/DMUL per amplitude issued one by one.
+            if (KB == 4 && dmma_min_pipe_ops() > 0 && pipe_ops >= dmma_min_pipe_ops()) {
+                std::vector<double> mat(2 * 256, 0.0);  // M[r][c], row-major complex
+                for (int c = 0; c < 16; ++c) {
+                    std::complex<double> v[16];
+                    v[c] = 1.0;
+                    for (int pi = 0; pi < od.nprim; ++pi) {
+                        const qsv_prim_desc& pd = prims[od.prim_begin + pi];
+                        const std::complex<double>* m = reinterpret_cast<const std::complex<double>*>(pool) + pd.mat_off;
+                        if (pd.kind == QSV_PRIM_CX) {
+                            for (int j = 0; j < 16; ++j)
+                                if ((j >> pd.a & 1) && !(j >> pd.b & 1))
+                                    std::swap(v[j], v[j | (1 << pd.b)]);
+                        } else if (pd.kind == QSV_PRIM_DIAG16) {
+                            for (int j = 0; j < 16; ++j)
+                                v[j] *= m[j];
+                        } else if (pd.kind == QSV_PRIM_U2) {
+                            const int A = 1 << pd.a, B = 1 << pd.b;
+                            for (int j = 0; j < 16; ++j) {
+                                if (j & (A | B))
+                                    continue;
+                                const std::complex<double> x[4] = {v[j], v[j | A], v[j | B], v[j | A | B]};
+                                std::complex<double> y[4];
+                                for (int r = 0; r < 4; ++r)
+                                    y[r] = m[4 * r] * x[0] + m[4 * r + 1] * x[1] + m[4 * r + 2] * x[2] + m[4 * r + 3] * x[3];
+                                v[j] = y[0];
+                                v[j | A] = y[1];
+                                v[j | B] = y[2];
+                                v[j | A | B] = y[3];
+                            }
+                        } else {  // U1 / U1R / U1I: the full 2x2 as given
+                            const int A = 1 << pd.a;
+                            for (int j = 0; j < 16; ++j) {
+                                if (j & A)
+                                    continue;
+                                const std::complex<double> x0 = v[j], x1 = v[j | A];
+                                v[j] = m[0] * x0 + m[1] * x1;
+                                v[j | A] = m[2] * x0 + m[3] * x1;
+                            }
+                        }
+                    }
+                    for (int r = 0; r < 16; ++r) {
+                        mat[2 * (16 * r + c)] = v[r].real();
+                        mat[2 * (16 * r + c) + 1] = v[r].imag();
+                    }
+                }
+                t.kind = QSV_OP_DMMA16;
+                t.nprim = 0;
+                pl.dprims.clear();
+                pl.pdata.clear();
+                pl.data = std::move(mat);
+                flops += 128.0 * amps * frac - prim_flops;
+            }
         } else if (od.kind == QSV_OP_PHASEPROD) {
             QSV_REQUIRE(od.k == 0, "op: PHASEPROD takes its qubits as FACTOR primitives (k = 0)");
             QSV_REQUIRE(od.prim_begin >= 0 && od.nprim >= 0 && od.prim_begin + od.nprim <= nprims,
@@ -909,7 +979,7 @@ int compile_pass(const qsv_step_desc& d, int n_total, int n_local, int rank,
         }
         std::sort(fix.begin(), fix.end());
         QSV_REQUIRE(fix.size() <= sizeof(t.fixpos), "op: too many fixed tile bits");
-        if (od.kind == QSV_OP_RBLOCK) {
+        if (t.kind == QSV_OP_RBLOCK) {
             // Lanes i = 0..7 of a quarter-warp own groups whose low free bits are
             // the lowest free tile positions.  The first `a` of them lie in tile
             // bits 0..2 (the SMEM bank bits of 16-B amplitudes); lanes that differ
