@@ -620,11 +620,15 @@ void relabel_columns(int K, const int32_t* rel, uint16_t* scol, uint16_t* dcol) 
 }
 
 // Minimum DFMA/DMUL count per amplitude of a 4-qubit register block's primitive list
-// for it to run as a dense DMMA16 op (QSV_DMMA_MIN_PIPE; 0 disables the tensor path).
+// for it to run as a dense DMMA16 op (QSV_DMMA_MIN_PIPE; 0, the default, keeps every block
+// on the DFMA primitives).  Measured on random-30: thresholds 32 / 40 / 56 give 420 / 303 /
+// 281 ms against 280 ms without, HEA-30 120 vs 115 ms: the dense form costs 128 flop per
+// amplitude where the primitive lists of these circuits cost 50-100, and the DMMA ops reach
+// ~21 TF (0.57 of the measured 37.1 TF) at 12 warps per SM (profiles/r02_kernel_ab.md).
 int dmma_min_pipe_ops() {
     static const int v = [] {
         const char* e = std::getenv("QSV_DMMA_MIN_PIPE");
-        return e ? std::atoi(e) : 40;
+        return e ? std::atoi(e) : 0;
     }();
     return v;
 }
