@@ -1321,14 +1321,18 @@ static Plan pack_ops(const Circuit& c, const std::vector<Op>& ops, const PlanOpt
         const bool remaining_only = std::getenv("QSV_VICTIM_REMAINING") != nullptr;
         while (done < nops) {
             int pick = -1;
-            // local ops that join the open pass first, then any local op
-            for (int i : ready)
-                if (is_local(i) && (pick < 0 || i < pick) && pk.fits(ops[i]))
-                    pick = i;
-            if (pick < 0)
+            // local ops that join the open pass first, then any local op; with
+            // list_schedule off the ops keep program order (the SURVEY §8e cross-P
+            // invariant: every P applies the same op sequence, bitwise equal results)
+            if (opt.list_schedule) {
                 for (int i : ready)
-                    if (is_local(i) && (pick < 0 || i < pick))
+                    if (is_local(i) && (pick < 0 || i < pick) && pk.fits(ops[i]))
                         pick = i;
+                if (pick < 0)
+                    for (int i : ready)
+                        if (is_local(i) && (pick < 0 || i < pick))
+                            pick = i;
+            }
             if (pick < 0) {
                 pick = *std::min_element(ready.begin(), ready.end());
                 const std::vector<int> need = local_needs(ops[pick]);

@@ -111,3 +111,31 @@ def test_two_rank_logical_swaps(tmp_path):
     assert all(p.exitcode == 0 for p in procs)
     err, nswaps = q.get(timeout=5)
     assert err < 1e-10
+
+
+@pytest.mark.parametrize("spec", ["random:12:6:2", "hea:11:3:4", "uccsd:10:200:3"])
+def test_program_order_plan_same_on_every_p(spec):
+    """with list scheduling off, the multi-rank planner applies the ops in program
+    order (swaps only in between), so every P sees the same op sequence as one GPU."""
+    from tests import dist_emulator as E
+    c = pkg.Circuit.generate(spec).fused(pkg.PlanOptions())
+    o = pkg.PlanOptions(fusion=False, list_schedule=False, relabel=0, register_blocks=False)
+
+    def seq(n_local):
+        steps, ops, prims, pool = E.export_plan(c, o, n_local)
+        out = []
+        for st in steps:
+            if st.kind != 0:
+                continue
+            for op in ops[st.op_begin:st.op_begin + st.op_count]:
+                d = {0: 1 << (2 * op.k), 1: 1 << op.k}.get(op.kind, 0)
+                out.append((op.kind, op.k, pool[op.mat_off:op.mat_off + d].tobytes()))
+        return out
+
+    one = seq(c.n)
+    for m in (1, 2):
+        got = seq(c.n - m)
+        assert got[:len(one)] == one
+        for kind, k, data in got[len(one):]:  # the final layout restore: exact permutations
+            v = np.frombuffer(data, dtype=np.complex128)
+            assert kind == 0 and set(np.unique(v)) <= {0, 1}
