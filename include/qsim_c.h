@@ -106,6 +106,7 @@ int qsim_engine_stats(qsim_engine* e, qsim_plan_stats* out);
 void* qsim_engine_stream(qsim_engine* e);      /* cudaStream_t */
 void* qsim_engine_qsv_state(qsim_engine* e);   /* qsv_state*   */
 void* qsim_engine_qsv_program(qsim_engine* e); /* qsv_program* */
+void* qsim_engine_qsv_ctx(qsim_engine* e);     /* qsv_ctx* (trace, abort)  */
 int qsim_engine_set_basis(qsim_engine* e, uint64_t global_index);
 int qsim_engine_upload(qsim_engine* e, const double* amps, uint64_t offset, uint64_t count);
 int qsim_engine_download(qsim_engine* e, double* amps, uint64_t offset, uint64_t count);

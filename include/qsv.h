@@ -84,6 +84,24 @@ int qsv_sync(qsv_ctx* ctx);
  * seconds (default 900).  qsv_ctx_aborted reports whether the context was aborted. */
 int qsv_ctx_abort(qsv_ctx* ctx, const char* reason);
 int qsv_ctx_aborted(qsv_ctx* ctx, int* out);
+
+/* PipelineTrace: with tracing on, every pass launch (per
+ * region when a swap is overlapped), P2P swap kernel, NCCL send/recv chunk and
+ * staging copy-back is bracketed by CUDA events on the stream it runs on.
+ * qsv_trace_enable(ctx, 1) clears the trace and sets the time origin (an event on the
+ * compute stream; CUDA-graph replay is bypassed while tracing); qsv_trace_read waits
+ * for the context's streams and writes up to cap records (*n = records available). */
+#define QSV_TRACE_PASS 0       /* pass kernel (chunk = region, -1 = whole shard)   */
+#define QSV_TRACE_SWAP 1       /* P2P swap kernel (chunk = region, -1 = whole)    */
+#define QSV_TRACE_SENDRECV 2   /* NCCL send/recv of one chunk (BBOP batch)        */
+#define QSV_TRACE_COPYBACK 3   /* copy-back / scatter of one received chunk       */
+#define QSV_TRACE_BARRIER 4    /* pairwise barrier of a P2P swap                  */
+typedef struct qsv_trace_rec {
+    int32_t kind, step, chunk, stream; /* stream: 0 compute, 1 comm, 2 copy */
+    double start_ms, end_ms;           /* relative to qsv_trace_enable     */
+} qsv_trace_rec;
+int qsv_trace_enable(qsv_ctx* ctx, int on);
+int qsv_trace_read(qsv_ctx* ctx, qsv_trace_rec* out, int cap, int* n);
 /* Thread-local description of the last failure on this thread. */
 const char* qsv_last_error(void);
 

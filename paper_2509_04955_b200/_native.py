@@ -64,6 +64,11 @@ class qsim_plan_opts(C.Structure):
     ]
 
 
+class qsv_trace_rec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("step", C.c_int32), ("chunk", C.c_int32), ("stream", C.c_int32),
+                ("start_ms", C.c_double), ("end_ms", C.c_double)]
+
+
 class qsim_plan_stats(C.Structure):
     _fields_ = [
         ("gates_in", C.c_int64),
@@ -110,7 +115,7 @@ def load_qsim() -> C.CDLL:
             raise QsvError(f"{p} missing: build the host library")
         L = C.CDLL(p)
         L.qsim_last_error.restype = C.c_char_p
-        for f in ("qsim_engine_stream", "qsim_engine_qsv_state", "qsim_engine_qsv_program"):
+        for f in ("qsim_engine_stream", "qsim_engine_qsv_state", "qsim_engine_qsv_program", "qsim_engine_qsv_ctx"):
             getattr(L, f).restype = C.c_void_p
             getattr(L, f).argtypes = [C.c_void_p]
         L.qsim_circuit_free.argtypes = [C.c_void_p]
@@ -419,6 +424,25 @@ class Engine:
         ms = (C.c_float * max(n, 1))()
         _check(load_qsim().qsim_engine_profile(self._h, ms), "profile")
         return [ms[i] for i in range(n)]
+
+    TRACE_KINDS = {0: "pass", 1: "swap", 2: "sendrecv", 3: "copyback", 4: "barrier"}
+
+    def trace_enable(self, on: bool = True):
+        """PipelineTrace: bracket every launch / swap chunk with CUDA events."""
+        _check(load_qsv().qsv_trace_enable(C.c_void_p(load_qsim().qsim_engine_qsv_ctx(self._h)), int(on)),
+               "qsv_trace_enable", load_qsv())
+
+    def trace(self) -> list[dict]:
+        """The trace since trace_enable: [{kind, step, chunk, stream, start_ms, end_ms}]."""
+        L = load_qsv()
+        ctx = C.c_void_p(load_qsim().qsim_engine_qsv_ctx(self._h))
+        n = C.c_int()
+        _check(L.qsv_trace_read(ctx, None, 0, C.byref(n)), "qsv_trace_read", L)
+        recs = (qsv_trace_rec * max(n.value, 1))()
+        _check(L.qsv_trace_read(ctx, recs, n.value, C.byref(n)), "qsv_trace_read", L)
+        return [{"kind": self.TRACE_KINDS.get(r.kind, str(r.kind)), "step": r.step, "chunk": r.chunk,
+                 "stream": ("compute", "comm", "copy")[r.stream], "start_ms": r.start_ms, "end_ms": r.end_ms}
+                for r in recs[:n.value]]
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:

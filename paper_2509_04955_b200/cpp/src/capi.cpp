@@ -371,6 +371,7 @@ int qsim_engine_stats(qsim_engine* e, qsim_plan_stats* out) {
 void* qsim_engine_stream(qsim_engine* e) { return e ? qsv_ctx_stream(e->ctx->get()) : nullptr; }
 void* qsim_engine_qsv_state(qsim_engine* e) { return e ? e->st->get() : nullptr; }
 void* qsim_engine_qsv_program(qsim_engine* e) { return e ? e->eng->program() : nullptr; }
+void* qsim_engine_qsv_ctx(qsim_engine* e) { return e ? e->ctx->get() : nullptr; }
 
 int qsim_engine_set_basis(qsim_engine* e, uint64_t idx) {
     return guard([&] {

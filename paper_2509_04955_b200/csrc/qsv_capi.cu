@@ -366,7 +366,63 @@ int wait_stream(qsv_ctx* ctx, cudaStream_t stream, const char* what) {
     }
 }
 
+int trace_open(qsv_ctx* ctx, int kind, int chunk, int stream_id, cudaStream_t s) {
+    if (!ctx->trace_on)
+        return -1;
+    qsv_ctx::TraceEv ev{kind, ctx->trace_step, chunk, stream_id, nullptr, nullptr};
+    if (cudaEventCreate(&ev.a) != cudaSuccess || cudaEventCreate(&ev.b) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    cudaEventRecord(ev.a, s);
+    ctx->trace.push_back(ev);
+    return static_cast<int>(ctx->trace.size()) - 1;
+}
+
+void trace_close(qsv_ctx* ctx, int idx, cudaStream_t s) {
+    if (idx >= 0 && idx < static_cast<int>(ctx->trace.size()))
+        cudaEventRecord(ctx->trace[idx].b, s);
+}
+
+void trace_clear(qsv_ctx* ctx) {
+    for (auto& e : ctx->trace) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    ctx->trace.clear();
+}
+
 } // namespace qsv
+
+extern "C" int qsv_trace_enable(qsv_ctx* ctx, int on) {
+    QSV_REQUIRE(ctx != nullptr, "qsv_trace_enable: null context");
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    qsv::trace_clear(ctx);
+    ctx->trace_on = on != 0;
+    if (ctx->trace_on) {
+        if (!ctx->trace_base)
+            QSV_CUDA(cudaEventCreate(&ctx->trace_base));
+        QSV_CUDA(cudaEventRecord(ctx->trace_base, ctx->stream));
+    }
+    return QSV_OK;
+}
+
+extern "C" int qsv_trace_read(qsv_ctx* ctx, qsv_trace_rec* out, int cap, int* n) {
+    QSV_REQUIRE(ctx != nullptr && n != nullptr && (out != nullptr || cap == 0), "qsv_trace_read: null argument");
+    QSV_CUDA(cudaSetDevice(ctx->device));
+    for (cudaStream_t s : {ctx->stream, ctx->comm_stream, ctx->copy_stream})
+        if (int rc = qsv::wait_stream(ctx, s, "qsv_trace_read"); rc != QSV_OK)
+            return rc;
+    *n = static_cast<int>(ctx->trace.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+        const auto& e = ctx->trace[i];
+        float a = 0, b = 0;
+        QSV_CUDA(cudaEventElapsedTime(&a, ctx->trace_base, e.a));
+        QSV_CUDA(cudaEventElapsedTime(&b, ctx->trace_base, e.b));
+        out[i] = qsv_trace_rec{e.kind, e.step, e.chunk, e.stream, a, b};
+    }
+    return QSV_OK;
+}
 
 extern "C" int qsv_ctx_abort(qsv_ctx* ctx, const char* reason) {
     QSV_REQUIRE(ctx != nullptr, "qsv_ctx_abort: null context");
@@ -395,6 +451,8 @@ extern "C" int qsv_ctx_destroy(qsv_ctx* ctx) {
     if (ctx->d_scratch) cudaFree(ctx->d_scratch);
     if (ctx->d_sync) cudaFree(ctx->d_sync);
     if (ctx->d_coll) cudaFree(ctx->d_coll);
+    qsv::trace_clear(ctx);
+    if (ctx->trace_base) cudaEventDestroy(ctx->trace_base);
     if (ctx->h_result) cudaFreeHost(ctx->h_result);
     cudaEventDestroy(ctx->ev_a);
     cudaEventDestroy(ctx->ev_b);
@@ -1309,11 +1367,18 @@ int env_int(const char* name, int dflt) {
 }
 
 cudaError_t launch_step(qsv_state* st, qsv_program* prog, size_t i, uint64_t rank_base,
-                        const qsv::LaunchRange& rg = qsv::LaunchRange{}) {
+                        const qsv::LaunchRange& rg = qsv::LaunchRange{}, int region = -1) {
     const qsv::Step& s = prog->steps[i];
+    qsv_ctx* ctx = st->ctx;
+    ctx->trace_step = static_cast<int>(i);
+    const int tr = qsv::trace_open(ctx, QSV_TRACE_PASS, region, 0, ctx->stream);
+    cudaError_t e;
     if (!prog->jit_of_step.empty() && prog->jit_of_step[i] >= 0)
-        return qsv::launch_jit(prog, st, i, prog->d_blobs + s.blob_off, rank_base, st->ctx->stream, rg);
-    return qsv::launch_pass(st, s, prog->d_blobs + s.blob_off, rank_base, st->ctx->stream, rg);
+        e = qsv::launch_jit(prog, st, i, prog->d_blobs + s.blob_off, rank_base, ctx->stream, rg);
+    else
+        e = qsv::launch_pass(st, s, prog->d_blobs + s.blob_off, rank_base, ctx->stream, rg);
+    qsv::trace_close(ctx, tr, ctx->stream);
+    return e;
 }
 
 uint64_t tile_mask(const qsv::Step& p) {
@@ -1411,6 +1476,7 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
             pre_start[kv.second.pre_begin] = kv.first;
     for (size_t i = 0; i < prog->steps.size(); ++i) {
         const qsv::Step& s = prog->steps[i];
+        ctx->trace_step = static_cast<int>(i);
         if (evs)
             QSV_CUDA(cudaEventRecord(evs[i], ctx->stream));
         auto ps = pre_start.find(i);
@@ -1426,12 +1492,13 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
                 qsv::LaunchRange rg = region_of(ov.rmask, c);
                 rg.sms = c > 0 ? ctx->sm_count - swap_sms : 0;
                 for (size_t p = i; p < w && err == cudaSuccess; ++p)
-                    err = launch_step(st, prog, p, rank_base, rg);
+                    err = launch_step(st, prog, p, rank_base, rg, static_cast<int>(c));
                 cudaEvent_t e;
                 cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
                 cudaEventRecord(e, ctx->stream);
                 pre_ev.push_back(e);
             }
+            ctx->trace_step = static_cast<int>(w);
             int rc = err == cudaSuccess ? qsv::run_swap(st, sw.desc.swap_global, sw.desc.swap_local, sw.desc.chunk_log2,
                                                         sw.desc.nbuf, &done, ov.rmask, &pre_ev)
                                         : QSV_E_CUDA;
@@ -1440,7 +1507,7 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
                 qsv::LaunchRange rg = region_of(ov.rmask, c);
                 rg.sms = c + 1 < done.size() ? ctx->sm_count - swap_sms : 0;
                 for (size_t p = w + 1; p <= ov.post_end && err == cudaSuccess; ++p)
-                    err = launch_step(st, prog, p, rank_base, rg);
+                    err = launch_step(st, prog, p, rank_base, rg, static_cast<int>(c));
             }
             qsv::join_swap(ctx);
             for (cudaEvent_t e : pre_ev)
@@ -1470,7 +1537,7 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
                     qsv::LaunchRange rg = region_of(it->second.rmask, c);
                     rg.sms = c + 1 < done.size() ? ctx->sm_count - swap_sms : 0;
                     for (size_t p = i + 1; p <= it->second.post_end && err == cudaSuccess; ++p)
-                        err = launch_step(st, prog, p, rank_base, rg);
+                        err = launch_step(st, prog, p, rank_base, rg, static_cast<int>(c));
                 }
                 qsv::join_swap(ctx);
                 for (cudaEvent_t e : done)
@@ -1508,7 +1575,7 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
                     rg.tile0 = c * (T / C);
                     rg.count = T / C;
                     rg.sms = c + 1 < C ? sms : 0;  // the last region runs after the transfers
-                    err = launch_step(st, prog, p, rank_base, rg);
+                    err = launch_step(st, prog, p, rank_base, rg, static_cast<int>(c));
                 }
             }
             qsv::join_swap(ctx);
@@ -1540,7 +1607,7 @@ extern "C" int qsv_program_run(qsv_state* st, qsv_program* prog) {
     if (int rc = qsv::check_aborted(ctx, "qsv_program_run"); rc != QSV_OK)
         return rc;
     QSV_CUDA(cudaSetDevice(ctx->device));
-    if (prog->has_collective || prog->steps.size() < 4)
+    if (prog->has_collective || prog->steps.size() < 4 || ctx->trace_on)
         return enqueue_steps(st, prog, nullptr);
     auto it = prog->graphs.find(st->amps);
     if (it == prog->graphs.end()) {

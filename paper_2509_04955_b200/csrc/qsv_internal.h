@@ -70,6 +70,16 @@ struct qsv_ctx {
     std::atomic<int> aborted{0};
     std::atomic<int> comm_aborted{0};
     std::string abort_reason;
+    // PipelineTrace: timing events around every pass launch, swap kernel,
+    // send/recv chunk and copy-back while tracing is on (qsv_trace_enable)
+    bool trace_on = false;
+    cudaEvent_t trace_base = nullptr;
+    struct TraceEv {
+        int32_t kind, step, chunk, stream;
+        cudaEvent_t a, b;
+    };
+    std::vector<TraceEv> trace;
+    int trace_step = -1;  // step being enqueued (read by the swap code)
 };
 
 struct qsv_state {
@@ -155,4 +165,8 @@ int wait_stream(qsv_ctx* ctx, cudaStream_t stream, const char* what);
 void abort_comm(qsv_ctx* ctx, const std::string& why);
 // QSV_E_NCCL with the abort reason when the context was aborted, else QSV_OK.
 int check_aborted(qsv_ctx* ctx, const char* what);
+// Trace records (no-ops unless tracing is on): open records an event on `s` before the
+// traced work and returns its index, close records the end event after it.
+int trace_open(qsv_ctx* ctx, int kind, int chunk, int stream_id, cudaStream_t s);
+void trace_close(qsv_ctx* ctx, int idx, cudaStream_t s);
 } // namespace qsv

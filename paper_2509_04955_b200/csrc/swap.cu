@@ -321,16 +321,22 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
         if (!fed) {
             cudaEventRecord(ctx->ev_a, ctx->stream);
             cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0);
+            const int tb0 = trace_open(ctx, QSV_TRACE_BARRIER, -1, 1, ctx->comm_stream);
             r = pair_barrier(ctx, peer);  // the peer's earlier passes are done
+            trace_close(ctx, tb0, ctx->comm_stream);
             if (r != ncclSuccess)
                 return fail_nccl("qsv_swap: barrier", r);
         }
         const uint64_t H = 1ull << (l - 1);
         const uint64_t half = H / 2;
         if (!chunk_done || region_mask == 0) {
+            const int tk = trace_open(ctx, QSV_TRACE_SWAP, -1, 1, ctx->comm_stream);
             p2p_swap_kernel<<<ctx->sm_count * 4, 256, 0, ctx->comm_stream>>>(st->amps, st->peer_amps[peer],
                                                                              a * half, half, v, sendbit, a);
+            trace_close(ctx, tk, ctx->comm_stream);
+            const int tb1 = trace_open(ctx, QSV_TRACE_BARRIER, -1, 1, ctx->comm_stream);
             r = pair_barrier(ctx, peer);  // the peer's writes into this shard are done
+            trace_close(ctx, tb1, ctx->comm_stream);
             if (r != ncclSuccess)
                 return fail_nccl("qsv_swap: barrier", r);
             if (chunk_done) {
@@ -364,9 +370,11 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
                 uint64_t rval = 0;
                 for (int i = 0; i < nr; ++i)
                     rval |= ((c >> i) & 1ull) << rb[i];
+                const int tk = trace_open(ctx, QSV_TRACE_SWAP, static_cast<int>(c), 1, ctx->comm_stream);
                 p2p_swap_region_kernel<<<sms * 4, 256, 0, ctx->comm_stream>>>(
                     st->amps, st->peer_amps[peer], a * mine_half, mine_half, pos[0], npos > 1 ? pos[1] : 0,
                     npos > 2 ? pos[2] : 0, npos, rval, sendbit << v, a << v);
+                trace_close(ctx, tk, ctx->comm_stream);
                 r = pair_barrier(ctx, peer);
                 if (r != ncclSuccess)
                     return fail_nccl("qsv_swap: barrier", r);
@@ -427,16 +435,19 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
                                                                  sendbit);
             src = send_stage + b * C;
         }
+        const int ts = trace_open(ctx, QSV_TRACE_SENDRECV, static_cast<int>(c), 1, ctx->comm_stream);
         ncclResult_t r = ncclGroupStart();
         if (r == ncclSuccess) r = ncclSend(src, 2 * C, ncclDouble, peer, ctx->comm, ctx->comm_stream);
         if (r == ncclSuccess) r = ncclRecv(recv_stage + b * C, 2 * C, ncclDouble, peer, ctx->comm, ctx->comm_stream);
         ncclResult_t r2 = ncclGroupEnd();
+        trace_close(ctx, ts, ctx->comm_stream);
         if (r != ncclSuccess || r2 != ncclSuccess) {
             rc = fail_nccl("qsv_swap: ncclSend/ncclRecv", r != ncclSuccess ? r : r2);
             break;
         }
         cudaEventRecord(recv_ev[b], ctx->comm_stream);
         cudaStreamWaitEvent(ctx->copy_stream, recv_ev[b], 0);
+        const int tc = trace_open(ctx, QSV_TRACE_COPYBACK, static_cast<int>(c), 2, ctx->copy_stream);
         if (contiguous) {
             e = cudaMemcpyAsync(dst_contig, recv_stage + b * C, C * sizeof(double2), cudaMemcpyDeviceToDevice,
                                 ctx->copy_stream);
@@ -446,6 +457,7 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
             scatter_half_kernel<<<grid, tb, 0, ctx->copy_stream>>>(st->amps, recv_stage + b * C, r0, C, v,
                                                                   sendbit);
         }
+        trace_close(ctx, tc, ctx->copy_stream);
         cudaEventRecord(free_ev[b], ctx->copy_stream);
         if (chunk_done) {
             // region c of the shard (half-index chunk c, both values of bit v) is final

@@ -146,3 +146,100 @@ def test_rank_failure_aborts_all_ranks(two, monkeypatch):
     monkeypatch.delenv("QSV_INJECT_FAIL_RANK")
     got, _ = run_dist(c, 1, 12, 2)  # the library is usable again afterwards
     assert np.abs(got - O.run_local(c)).max() <= 1e-10
+
+
+def _engines_in_threads(c, opts, nranks):
+    """One Engine per GPU, created from one thread each (the communicator init is collective)."""
+    import threading
+    cid = pkg.Engine.comm_unique_id()
+    engines = [None] * nranks
+    errs = []
+
+    def make(r):
+        try:
+            engines[r] = pkg.Engine(c, opts, device=r, rank=r, nranks=nranks, comm_id=cid)
+        except Exception as ex:  # pragma: no cover - surfaced below
+            errs.append(ex)
+
+    th = [threading.Thread(target=make, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    return engines
+
+
+def _run_all(engines, fn):
+    import threading
+    th = [threading.Thread(target=fn, args=(e,)) for e in engines]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+
+
+@pytest.mark.timeout(600)
+def test_pipeline_trace_nccl_chunks(two, monkeypatch):
+    """SPEC:352-356 / :387 / :411 on the chunked NCCL swap (B = 2 staging buffers): every
+    chunk of the half-space is sent exactly once per swap (batch completeness), the copy-back
+    of chunk i overlaps the transfer of chunk i+1 (Table 2 'With Buff'), and a staging buffer
+    is never a receive target while its previous chunk is still being copied back (buffer
+    safety: recv(i + B) starts after copy-back(i) ends)."""
+    monkeypatch.setenv("QSV_SWAP_MODE", "nccl")
+    c = pkg.Circuit.generate("random:26:6:2")
+    B = 2
+    engines = _engines_in_threads(c, pkg.PlanOptions(chunk_log2=20, nbuf=B), 2)
+    try:
+        def go(e):
+            e.trace_enable(True)
+            e.set_basis(0)
+            e.run()
+            e.sync()
+        _run_all(engines, go)
+        tr = engines[0].trace()
+    finally:
+        for e in engines:
+            e.close()
+    swaps = sorted({r["step"] for r in tr if r["kind"] == "sendrecv"})
+    assert swaps, "no swap in the plan"
+    nchunks = 1 << (c.n - 1 - 1 - 20)  # half of the 2^25-amplitude shard in 2^20 chunks
+    overlapped = 0
+    for s in swaps:
+        sr = sorted((r for r in tr if r["step"] == s and r["kind"] == "sendrecv"), key=lambda r: r["chunk"])
+        cb = sorted((r for r in tr if r["step"] == s and r["kind"] == "copyback"), key=lambda r: r["chunk"])
+        assert [r["chunk"] for r in sr] == list(range(nchunks)) == [r["chunk"] for r in cb]
+        for i in range(nchunks):
+            assert cb[i]["start_ms"] >= sr[i]["end_ms"] - 1e-3  # a chunk is copied back after it landed
+            if i + B < nchunks:
+                assert sr[i + B]["start_ms"] >= cb[i]["end_ms"] - 1e-3  # buffer safety
+            if i + 1 < nchunks and cb[i]["start_ms"] < sr[i + 1]["end_ms"] and cb[i]["end_ms"] > sr[i + 1]["start_ms"]:
+                overlapped += 1
+    assert overlapped >= (nchunks - 1) * len(swaps) // 2, f"only {overlapped} copy-backs overlapped a transfer"
+
+
+@pytest.mark.timeout(600)
+def test_pipeline_trace_p2p(two):
+    """The default NVLink P2P swap: one kernel per swap bracketed by the two pair barriers."""
+    c = pkg.Circuit.generate("random:24:6:2")
+    engines = _engines_in_threads(c, pkg.PlanOptions(), 2)
+    try:
+        def go(e):
+            e.trace_enable(True)
+            e.set_basis(0)
+            e.run()
+            e.sync()
+        _run_all(engines, go)
+        tr = engines[0].trace()
+    finally:
+        for e in engines:
+            e.close()
+    sw = [r for r in tr if r["kind"] == "swap"]
+    bars = [r for r in tr if r["kind"] == "barrier"]
+    passes = [r for r in tr if r["kind"] == "pass"]
+    assert sw and len(bars) == 2 * len(sw) and passes
+    for k in sw:
+        before = [b for b in bars if b["step"] == k["step"] and b["end_ms"] <= k["start_ms"] + 1e-3]
+        after = [b for b in bars if b["step"] == k["step"] and b["start_ms"] >= k["end_ms"] - 1e-3]
+        assert before and after
