@@ -159,6 +159,12 @@ int qsim_peer_rank(int r, int t, int l, int* out);
  * gathers all 2^n amplitudes into amps (host). */
 int qsim_run_distributed(const qsim_circuit* c, int m, int b, int buffers, const int* devices,
                          const qsim_plan_opts* opts, double* amps, qsim_dist_report* report);
+/* The same run without a gather: rank r writes its shard to
+ * <dir>/shard_r<r>_of_<R>.bin (complex128 LE, global indices [r 2^l, (r+1) 2^l)) and
+ * <dir>/manifest.json is written.  qsim_run_distributed refuses states above the
+ * single-host cap QSV_GATHER_CAP_GIB (default 64) with QSV_E_ARG. */
+int qsim_run_distributed_files(const qsim_circuit* c, int m, int b, int buffers, const int* devices,
+                               const qsim_plan_opts* opts, const char* dir, qsim_dist_report* report);
 
 /* ---- memtrack (ref memtrack.hpp:12-26) scripted session, for parity tests ----
  * ops[2*i] = kind (0 enable, 1 register_thread, 2 set_phase, 3 on_alloc,

@@ -101,6 +101,16 @@ typedef struct qsv_trace_rec {
     double start_ms, end_ms;           /* relative to qsv_trace_enable     */
 } qsv_trace_rec;
 int qsv_trace_enable(qsv_ctx* ctx, int on);
+/* Instrumented device memory of a context (the SPEC:397 / :573 memory audit): every
+ * device allocation the library makes for the context (state shard, swap staging,
+ * program blobs, collective and reduction scratch) is counted; qsv_ctx_mem reports the
+ * live bytes and the high-water mark since creation or the last reset.  An optional hook
+ * sees every allocation (+bytes) and release (-bytes) on the calling thread; kind:
+ * 0 state, 1 swap staging, 2 program, 3 scratch. */
+typedef void (*qsv_alloc_hook)(void* user, int64_t delta_bytes, int kind);
+int qsv_ctx_set_alloc_hook(qsv_ctx* ctx, qsv_alloc_hook hook, void* user);
+int qsv_ctx_mem(qsv_ctx* ctx, size_t* live_bytes, size_t* peak_bytes);
+int qsv_ctx_mem_reset_peak(qsv_ctx* ctx);
 int qsv_trace_read(qsv_ctx* ctx, qsv_trace_rec* out, int cap, int* n);
 /* Thread-local description of the last failure on this thread. */
 const char* qsv_last_error(void);

@@ -10,6 +10,7 @@
 #include "qsim/planner.hpp"
 #include "qsim/statevector.hpp"
 
+#include <string>
 #include <vector>
 
 namespace qsim {
@@ -18,8 +19,23 @@ struct DistributedReport {
     int ranks = 1;
     std::size_t swaps = 0;
     double seconds = 0.0;             // wall time of the simulation (all ranks)
-    std::vector<std::size_t> peak_bytes;  // per-rank device bytes (state + staging)
+    // per-rank high-water mark of the library's device allocations (state shard, swap
+    // staging, program blobs, scratch), instrumented through qsv_ctx_mem
+    std::vector<std::size_t> peak_bytes;
+    std::vector<std::string> files;   // run_distributed_to_files: one shard file per rank
 };
+
+// Largest state (bytes) run_distributed gathers to one host: QSV_GATHER_CAP_GIB
+// (default 64 GiB).  Larger states are refused there; run_distributed_to_files writes one
+// file per rank instead.
+std::size_t gather_cap_bytes();
+
+// Same simulation as run_distributed, but each rank writes its shard (global indices
+// [r 2^l, (r+1) 2^l), interleaved little-endian fp64 re/im) to <dir>/shard_r<r>_of_<R>.bin
+// and rank 0 writes <dir>/manifest.json; nothing is gathered.
+void run_distributed_to_files(const Circuit& c, const PartitionPlan& plan, const std::string& dir,
+                              const std::vector<int>& devices = {}, DistributedReport* report = nullptr,
+                              const PlanOptions& opt = PlanOptions{});
 
 // Simulates `c` from |0...0> over plan.ranks() GPUs (devices[r] for rank r,
 // default 0..ranks-1) and gathers the state to rank 0's host StateVector.

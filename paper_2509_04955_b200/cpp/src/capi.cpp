@@ -612,6 +612,27 @@ int qsim_run_distributed(const qsim_circuit* c, int m, int b, int buffers, const
     });
 }
 
+int qsim_run_distributed_files(const qsim_circuit* c, int m, int b, int buffers, const int* devices,
+                               const qsim_plan_opts* opts, const char* dir, qsim_dist_report* report) {
+    return guard([&] {
+        REQUIRE(c && dir, "qsim_run_distributed_files: null argument");
+        const qsim::PartitionPlan p(c->c.n, m, b, buffers);
+        std::vector<int> dev;
+        if (devices)
+            dev.assign(devices, devices + p.ranks());
+        qsim::DistributedReport rep;
+        qsim::run_distributed_to_files(c->c, p, dir, dev, &rep, to_opts(opts));
+        if (report) {
+            report->ranks = rep.ranks;
+            report->swaps = static_cast<int64_t>(rep.swaps);
+            report->seconds = rep.seconds;
+            for (std::size_t r = 0; r < rep.peak_bytes.size() && r < 64; ++r)
+                report->peak_bytes[r] = static_cast<int64_t>(rep.peak_bytes[r]);
+        }
+        return QSV_OK;
+    });
+}
+
 void qsim_memtrack_script(const long long* ops, int nops, int nranks, unsigned long long* peaks) {
     using namespace qsim::memtrack;
     for (int i = 0; i < nops; ++i) {

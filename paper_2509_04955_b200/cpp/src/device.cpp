@@ -17,9 +17,22 @@ void qsv_check(int rc, const std::string& what) {
     throw std::runtime_error(msg + " (qsv code " + std::to_string(rc) + ")");
 }
 
+namespace {
+// Every device allocation of the library for this context, as it happens, on the
+// calling thread's memtrack rank/phase (ref memtrack.hpp:20-21): the instrumented
+// BBOP memory audit.
+void memtrack_hook(void*, int64_t delta, int) {
+    if (delta >= 0)
+        memtrack::on_alloc(static_cast<std::size_t>(delta));
+    else
+        memtrack::on_free(static_cast<std::size_t>(-delta));
+}
+} // namespace
+
 DeviceContext::DeviceContext(int device, int rank, int nranks, const void* comm_id)
     : rank_(rank), nranks_(nranks) {
     qsv_check(qsv_ctx_create(device, rank, nranks, comm_id, &ctx_), "rank " + std::to_string(rank) + ": qsv_ctx_create");
+    qsv_ctx_set_alloc_hook(ctx_, memtrack_hook, nullptr);
 }
 
 DeviceContext::~DeviceContext() { qsv_ctx_destroy(ctx_); }
@@ -34,14 +47,10 @@ DeviceContext& DeviceContext::default_context() {
 }
 
 DeviceState::DeviceState(DeviceContext& ctx, int n_local) : ctx_(ctx), n_local_(n_local) {
-    qsv_check(qsv_state_alloc(ctx.get(), n_local, &st_, &bytes_), "qsv_state_alloc");
-    memtrack::on_alloc(bytes_);
+    qsv_check(qsv_state_alloc(ctx.get(), n_local, &st_, &bytes_), "qsv_state_alloc");  // memtrack via the hook
 }
 
-DeviceState::~DeviceState() {
-    qsv_state_free(st_);
-    memtrack::on_free(bytes_);
-}
+DeviceState::~DeviceState() { qsv_state_free(st_); }
 
 void DeviceState::set_basis(Index global_index) {
     qsv_check(qsv_state_set_basis(st_, global_index), "qsv_state_set_basis");

@@ -186,8 +186,8 @@ int ensure_partials(qsv_ctx* ctx) {
     if (ctx->partials_cap >= need)
         return QSV_OK;
     if (ctx->d_partials)
-        cudaFree(ctx->d_partials);
-    QSV_CUDA(cudaMalloc(&ctx->d_partials, need * sizeof(double)));
+        qsv::dev_free(ctx, ctx->d_partials, 3);
+    QSV_CUDA(qsv::dev_alloc(ctx, reinterpret_cast<void**>(&ctx->d_partials), need * sizeof(double), 3));
     ctx->partials_cap = need;
     return QSV_OK;
 }
@@ -275,8 +275,10 @@ extern "C" int qsv_ctx_create(int device, int rank, int nranks, const void* comm
         // local allocations first; the init is joined whatever their outcome (the peers
         // are already inside it) and a rank whose allocations failed aborts right after,
         // so the others see an async error instead of waiting forever
-        const cudaError_t ea = cudaMalloc(&ctx->d_coll, 128 * static_cast<size_t>(nranks) + 64);
-        const cudaError_t eb = ea == cudaSuccess ? cudaMalloc(&ctx->d_sync, 2 * sizeof(double)) : ea;
+        const cudaError_t ea = qsv::dev_alloc(ctx, reinterpret_cast<void**>(&ctx->d_coll),
+                                              128 * static_cast<size_t>(nranks) + 64, 3);
+        const cudaError_t eb =
+            ea == cudaSuccess ? qsv::dev_alloc(ctx, reinterpret_cast<void**>(&ctx->d_sync), 2 * sizeof(double), 3) : ea;
         if (eb == cudaSuccess)
             cudaMemset(ctx->d_sync, 0, 2 * sizeof(double));
         cudaGetLastError();
@@ -366,6 +368,34 @@ int wait_stream(qsv_ctx* ctx, cudaStream_t stream, const char* what) {
     }
 }
 
+cudaError_t dev_alloc(qsv_ctx* ctx, void** p, size_t bytes, int kind) {
+    const cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess)
+        return e;
+    ctx->mem_sizes[*p] = bytes;
+    const size_t cur = ctx->mem_cur += bytes;
+    size_t pk = ctx->mem_peak.load();
+    while (cur > pk && !ctx->mem_peak.compare_exchange_weak(pk, cur)) {
+    }
+    if (ctx->alloc_hook)
+        ctx->alloc_hook(ctx->alloc_user, static_cast<int64_t>(bytes), kind);
+    return e;
+}
+
+void dev_free(qsv_ctx* ctx, void* p, int kind) {
+    if (!p)
+        return;
+    cudaFree(p);
+    auto it = ctx->mem_sizes.find(p);
+    if (it == ctx->mem_sizes.end())
+        return;
+    const size_t bytes = it->second;
+    ctx->mem_sizes.erase(it);
+    ctx->mem_cur -= bytes;
+    if (ctx->alloc_hook)
+        ctx->alloc_hook(ctx->alloc_user, -static_cast<int64_t>(bytes), kind);
+}
+
 int trace_open(qsv_ctx* ctx, int kind, int chunk, int stream_id, cudaStream_t s) {
     if (!ctx->trace_on)
         return -1;
@@ -393,6 +423,28 @@ void trace_clear(qsv_ctx* ctx) {
 }
 
 } // namespace qsv
+
+extern "C" int qsv_ctx_set_alloc_hook(qsv_ctx* ctx, qsv_alloc_hook hook, void* user) {
+    QSV_REQUIRE(ctx != nullptr, "qsv_ctx_set_alloc_hook: null context");
+    ctx->alloc_hook = hook;
+    ctx->alloc_user = user;
+    return QSV_OK;
+}
+
+extern "C" int qsv_ctx_mem(qsv_ctx* ctx, size_t* live_bytes, size_t* peak_bytes) {
+    QSV_REQUIRE(ctx != nullptr, "qsv_ctx_mem: null context");
+    if (live_bytes)
+        *live_bytes = ctx->mem_cur.load();
+    if (peak_bytes)
+        *peak_bytes = ctx->mem_peak.load();
+    return QSV_OK;
+}
+
+extern "C" int qsv_ctx_mem_reset_peak(qsv_ctx* ctx) {
+    QSV_REQUIRE(ctx != nullptr, "qsv_ctx_mem_reset_peak: null context");
+    ctx->mem_peak = ctx->mem_cur.load();
+    return QSV_OK;
+}
 
 extern "C" int qsv_trace_enable(qsv_ctx* ctx, int on) {
     QSV_REQUIRE(ctx != nullptr, "qsv_trace_enable: null context");
@@ -446,11 +498,11 @@ extern "C" int qsv_ctx_destroy(qsv_ctx* ctx) {
         qsv::wait_stream(ctx, ctx->stream, "qsv_ctx_destroy");
     if (ctx->comm && !ctx->comm_aborted.load())
         ncclCommDestroy(ctx->comm);
-    if (ctx->d_partials) cudaFree(ctx->d_partials);
-    if (ctx->d_stage) cudaFree(ctx->d_stage);
-    if (ctx->d_scratch) cudaFree(ctx->d_scratch);
-    if (ctx->d_sync) cudaFree(ctx->d_sync);
-    if (ctx->d_coll) cudaFree(ctx->d_coll);
+    qsv::dev_free(ctx, ctx->d_partials, 3);
+    qsv::dev_free(ctx, ctx->d_stage, 1);
+    qsv::dev_free(ctx, ctx->d_scratch, 3);
+    qsv::dev_free(ctx, ctx->d_sync, 3);
+    qsv::dev_free(ctx, ctx->d_coll, 3);
     qsv::trace_clear(ctx);
     if (ctx->trace_base) cudaEventDestroy(ctx->trace_base);
     if (ctx->h_result) cudaFreeHost(ctx->h_result);
@@ -489,7 +541,7 @@ extern "C" int qsv_state_alloc(qsv_ctx* ctx, int n_local, qsv_state** out, size_
     st->n_local = n_local;
     st->size = 1ull << n_local;
     const size_t b = sizeof(double2) * st->size;
-    cudaError_t e = cudaMalloc(&st->amps, b);
+    cudaError_t e = qsv::dev_alloc(ctx, reinterpret_cast<void**>(&st->amps), b, 0);
     if (e != cudaSuccess) {
         delete st;
         set_error("qsv_state_alloc: cudaMalloc of " + std::to_string(b) + " bytes failed: " +
@@ -511,7 +563,7 @@ extern "C" int qsv_state_free(qsv_state* st) {
     for (size_t q = 0; q < st->peer_amps.size(); ++q)
         if (st->peer_ipc[q] && st->peer_amps[q])
             cudaIpcCloseMemHandle(st->peer_amps[q]);
-    cudaFree(st->amps);
+    qsv::dev_free(st->ctx, st->amps, 0);
     delete st;
     return QSV_OK;
 }
@@ -1189,7 +1241,7 @@ extern "C" int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local, const 
         prog->steps.push_back(s);
     }
     if (!all.empty()) {
-        cudaError_t e = cudaMalloc(&prog->d_blobs, all.size());
+        cudaError_t e = qsv::dev_alloc(ctx, reinterpret_cast<void**>(&prog->d_blobs), all.size(), 2);
         if (e != cudaSuccess) {
             delete prog;
             set_error(std::string("qsv_program_create: cudaMalloc: ") + cudaGetErrorString(e));
@@ -1197,7 +1249,7 @@ extern "C" int qsv_program_create(qsv_ctx* ctx, int n_total, int n_local, const 
         }
         e = cudaMemcpy(prog->d_blobs, all.data(), all.size(), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
-            cudaFree(prog->d_blobs);
+            qsv::dev_free(ctx, prog->d_blobs, 2);
             delete prog;
             set_error(std::string("qsv_program_create: upload: ") + cudaGetErrorString(e));
             return QSV_E_CUDA;
@@ -1306,7 +1358,7 @@ extern "C" int qsv_program_free(qsv_program* prog) {
         cudaGraphExecDestroy(kv.second);
     qsv::jit_release(prog);
     if (prog->d_blobs)
-        cudaFree(prog->d_blobs);
+        qsv::dev_free(prog->ctx, prog->d_blobs, 2);
     delete prog;
     return QSV_OK;
 }
@@ -1751,10 +1803,11 @@ extern "C" int qsv_max_abs_diff(qsv_state* st, const double* host_ref, uint64_t 
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << 26);  // 1 GiB staging at most
     if (ctx->scratch_bytes < chunk * sizeof(double2)) {
         if (ctx->d_scratch)
-            cudaFree(ctx->d_scratch);
+            qsv::dev_free(ctx, ctx->d_scratch, 3);
         ctx->d_scratch = nullptr;
         ctx->scratch_bytes = 0;
-        QSV_CUDA(cudaMalloc(&ctx->d_scratch, std::max<uint64_t>(chunk, 1) * sizeof(double2)));
+        QSV_CUDA(qsv::dev_alloc(ctx, reinterpret_cast<void**>(&ctx->d_scratch),
+                                std::max<uint64_t>(chunk, 1) * sizeof(double2), 3));
         ctx->scratch_bytes = std::max<uint64_t>(chunk, 1) * sizeof(double2);
     }
     double worst = 0.0;

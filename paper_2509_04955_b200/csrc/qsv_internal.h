@@ -80,6 +80,13 @@ struct qsv_ctx {
     };
     std::vector<TraceEv> trace;
     int trace_step = -1;  // step being enqueued (read by the swap code)
+    // instrumented device memory: every cudaMalloc/cudaFree of the
+    // library goes through qsv::dev_alloc / dev_free, which keep these counters and call
+    // the caller's hook (qsim feeds memtrack from it)
+    std::atomic<size_t> mem_cur{0}, mem_peak{0};
+    std::map<void*, size_t> mem_sizes;
+    qsv_alloc_hook alloc_hook = nullptr;
+    void* alloc_user = nullptr;
 };
 
 struct qsv_state {
@@ -165,6 +172,9 @@ int wait_stream(qsv_ctx* ctx, cudaStream_t stream, const char* what);
 void abort_comm(qsv_ctx* ctx, const std::string& why);
 // QSV_E_NCCL with the abort reason when the context was aborted, else QSV_OK.
 int check_aborted(qsv_ctx* ctx, const char* what);
+// Device allocations of a context (counted, reported to the context's hook).
+cudaError_t dev_alloc(qsv_ctx* ctx, void** p, size_t bytes, int kind);
+void dev_free(qsv_ctx* ctx, void* p, int kind);
 // Trace records (no-ops unless tracing is on): open records an event on `s` before the
 // traced work and returns its index, close records the end event after it.
 int trace_open(qsv_ctx* ctx, int kind, int chunk, int stream_id, cudaStream_t s);

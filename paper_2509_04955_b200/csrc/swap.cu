@@ -310,7 +310,7 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
     }
     if (p2p_mode() && st->peer_amps.size() == static_cast<size_t>(ctx->nranks) && st->peer_amps[peer]) {
         if (!ctx->d_sync) {
-            e = cudaMalloc(&ctx->d_sync, 2 * sizeof(double));
+            e = dev_alloc(ctx, reinterpret_cast<void**>(&ctx->d_sync), 2 * sizeof(double), 3);
             if (e != cudaSuccess)
                 return fail_cuda("qsv_swap: sync token cudaMalloc", e);
             cudaMemset(ctx->d_sync, 0, 2 * sizeof(double));
@@ -397,10 +397,10 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
         if (int rc = wait_stream(ctx, ctx->copy_stream, "qsv_swap: staging resize"); rc != QSV_OK)
             return rc;
         if (ctx->d_stage)
-            cudaFree(ctx->d_stage);
+            dev_free(ctx, ctx->d_stage, 1);
         ctx->d_stage = nullptr;
         ctx->stage_bytes = 0;
-        e = cudaMalloc(&ctx->d_stage, need);
+        e = dev_alloc(ctx, &ctx->d_stage, need, 1);
         if (e != cudaSuccess)
             return fail_cuda("qsv_swap: staging cudaMalloc", e);
         ctx->stage_bytes = need;

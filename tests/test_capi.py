@@ -1,3 +1,4 @@
+import numpy as np
 """The C-ABI libraries load and export every function their headers declare
 (no compute calls: runs without a GPU)."""
 import ctypes as C
@@ -94,3 +95,16 @@ def test_plan_export_capacity_checked():
     rc = L.qsim_plan_export(c._h, C.byref(o), 12, C.byref(ns), C.byref(no), C.byref(npr), C.byref(pl),
                             None, ops, None, None)
     assert rc != 0 and no.value == need
+
+
+def test_gather_cap_refused_without_gpu(monkeypatch):
+    """a state above the single-host cap is not gathered (checked before any GPU work)."""
+    import ctypes as C
+    import paper_2509_04955_b200 as pkg
+    monkeypatch.setenv("QSV_GATHER_CAP_GIB", "0.000001")
+    c = pkg.Circuit.generate("qft:12")
+    out = np.zeros(1 << 12, dtype=np.complex128)
+    o = pkg.PlanOptions().to_c()
+    rc = pkg.load_qsim().qsim_run_distributed(c._h, 1, 8, 2, None, C.byref(o),
+                                              out.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), None)
+    assert rc != 0 and b"cap" in pkg.load_qsim().qsim_last_error()
