@@ -100,6 +100,19 @@ struct GeomArg {
     int32_t nreg;
     int32_t reg[3];
     uint64_t rval;
+    // Fused qubit swap (BBOP over NVLink P2P, swap.cu / pass_pipeline): with `peer` set,
+    // the pass runs on the layout AFTER swapping the global qubit of bit value `sgbit`
+    // into local bit `sv`: the half of each tile (sv_tile = 1: sv is a high tile bit) or
+    // the tiles (sv_tile = 0) whose bit sv differs from sgbit are read from the peer's
+    // shard at index ^ (1 << sv); results are stored locally.  Before storing into a slot
+    // the peer still has to read, a CTA waits for its twin (same blockIdx, same
+    // iteration on the peer) to flag that its loads landed.
+    const double2* peer;
+    unsigned long long* flag_mine;  // written by the peer's twins
+    unsigned long long* flag_peer;  // this rank's twins write here
+    uint64_t epoch;                 // flag value of iteration i: (epoch << 32) | (i + 1)
+    int32_t sv, sv_tile, sv_tidx;   // sv_tidx (sv_tile = 0): tile-index bit of sv
+    uint32_t sgbit;
 };
 
 // Largest per-pass blob (bytes of shared memory on top of the tile buffers).

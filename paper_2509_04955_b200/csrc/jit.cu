@@ -833,6 +833,16 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
     ga.nhigh = s.geom.nhigh;
     for (int i = 0; i < s.geom.nhigh; ++i)
         ga.high[i] = s.geom.high[i];
+    if (rg.fuse) {
+        ga.peer = rg.fuse->peer;
+        ga.flag_mine = rg.fuse->flag_mine;
+        ga.flag_peer = rg.fuse->flag_peer;
+        ga.epoch = rg.fuse->epoch;
+        ga.sv = rg.fuse->sv;
+        ga.sv_tile = rg.fuse->sv_tile;
+        ga.sv_tidx = rg.fuse->sv_tidx;
+        ga.sgbit = rg.fuse->sgbit;
+    }
     const uint64_t all_tiles = st->size >> s.geom.K;
     const uint64_t region_tiles = apply_region(ga, rg, all_tiles);
     ga.tile0 = std::min(rg.tile0, region_tiles);
@@ -841,7 +851,9 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
         return cudaSuccess;
     const int sms = rg.sms > 0 ? std::min(rg.sms, st->ctx->sm_count) : st->ctx->sm_count;
     const uint64_t ctas_needed = (tiles + jk.mt - 1) / jk.mt;
-    const uint64_t grid = std::min<uint64_t>(ctas_needed, static_cast<uint64_t>(per_sm) * sms);
+    uint64_t grid = std::min<uint64_t>(ctas_needed, static_cast<uint64_t>(per_sm) * sms);
+    if (rg.fuse)  // one flag per CTA (kFlagBytes)
+        grid = std::min<uint64_t>(grid, kFlagBytes / sizeof(unsigned long long));
     double2* psi = st->amps;
     uint32_t bb = s.blob_bytes;
     uint64_t rb = rank_base, nt = tiles;

@@ -790,8 +790,8 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     // High qubits that continue the low run (high[i] == L + i) are contiguous in
     // HBM too: merge them into the bulk copies (fewer, longer TMA runs).
     int m = 0;
-    while (m < geom.nhigh && geom.high[m] == L + m)
-        ++m;
+    while (m < geom.nhigh && geom.high[m] == L + m && !(geom.peer && geom.sv_tile && geom.high[m] == geom.sv))
+        ++m;  // (a fused swap's bit sv must separate runs: its two halves have different sources)
     const int RL = L + m;
     const int nruns = nh >> m;
     const uint32_t run_bytes = static_cast<uint32_t>(sizeof(double2)) << RL;
@@ -822,7 +822,15 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     const int warp = static_cast<int>(QSV_LTID >> 5);
     const bool issuer = warp < NW;
     const int my_runs = nruns > warp ? (nruns - warp + NW - 1) / NW : 0;
-    auto tile_of = [&](uint64_t T) { return T * MT + static_cast<uint64_t>(sub); };
+    // fused swap: whole-tile mode pairs tile t on the ranks with sgbit = 0 with tile
+    // t ^ (1 << sv_tidx) on their peers, so the twins of an iteration are partner tiles
+    const bool fused = geom.peer != nullptr;
+    const uint64_t txor = (fused && !geom.sv_tile && geom.sgbit) ? (1ull << geom.sv_tidx) : 0ull;
+    const uint64_t svm = fused ? (1ull << geom.sv) : 0ull;
+    const uint64_t sgm = fused && geom.sgbit ? svm : 0ull;
+    auto tile_of = [&](uint64_t T) { return (T * MT + static_cast<uint64_t>(sub)) ^ txor; };
+    // does this tile read (whole mode) or hold (mixed mode) data of the peer?
+    auto remote_tile = [&](uint64_t base) { return fused && (geom.sv_tile || (base & svm) != sgm); };
     auto issue_load = [&](uint64_t t, int b) {
         const uint64_t base = tile_base(geom.tile0 + t, geom);
         double2* dst = bufs + b * TILE;
@@ -831,7 +839,11 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         __syncwarp();
         for (int k = lane; k < my_runs; k += 32) {
             const int j = warp + NW * k;
-            bulk_load(dst + (j << RL), psi + base + hi_off[j << m], run_bytes, &mbar[b]);
+            const uint64_t idx = base + hi_off[j << m];
+            const double2* src = psi + idx;
+            if (fused && (idx & svm) != sgm)
+                src = geom.peer + (idx ^ svm);  // NVLink: the peer's slot of this amplitude run
+            bulk_load(dst + (j << RL), src, run_bytes, &mbar[b]);
         }
     };
 
@@ -865,6 +877,11 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         double2* tile = bufs + b * TILE;
         const uint64_t base = valid ? tile_base(geom.tile0 + t, geom) : 0;
         const uint64_t full_base = rank_base | base;
+        const bool remote = valid && remote_tile(base);
+        const unsigned long long flag_val = (static_cast<unsigned long long>(geom.epoch) << 32) | (it + 1u);
+        if (remote && threadIdx.x == 0)  // this CTA has read the peer's slots of the tile
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(geom.flag_peer + blockIdx.x), "l"(flag_val)
+                         : "memory");
         if (MT > 1 && !valid && issuer)
             bulk_wait_read_all();  // the stale buffer may still feed a store; every op starts with a CTA barrier
 
@@ -874,6 +891,20 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         fence_proxy_async();
         __syncthreads();
         if (issuer && valid) {
+            if (remote) {
+                // the slots we overwrite are the peer's source for its twin tile: wait until
+                // the twin's loads have landed (it flags the same iteration)
+                if (lane == 0) {
+                    unsigned long long seen;
+                    do {
+                        asm volatile("ld.acquire.sys.global.u64 %0, [%1];"
+                                     : "=l"(seen)
+                                     : "l"(geom.flag_mine + blockIdx.x)
+                                     : "memory");
+                    } while (seen < flag_val);
+                }
+                __syncwarp();
+            }
             for (int k = lane; k < my_runs; k += 32) {
                 const int j = warp + NW * k;
                 bulk_store(psi + base + hi_off[j << m], tile + (j << RL), run_bytes);

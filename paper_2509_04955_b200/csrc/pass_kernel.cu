@@ -126,13 +126,25 @@ cudaError_t launch_variant(const qsv_state* st, const Step& step, const unsigned
     for (int i = 0; i < step.geom.nhigh; ++i)
         ga.high[i] = step.geom.high[i];
     const uint64_t all_tiles = st->size >> K;
+    if (rg.fuse) {
+        ga.peer = rg.fuse->peer;
+        ga.flag_mine = rg.fuse->flag_mine;
+        ga.flag_peer = rg.fuse->flag_peer;
+        ga.epoch = rg.fuse->epoch;
+        ga.sv = rg.fuse->sv;
+        ga.sv_tile = rg.fuse->sv_tile;
+        ga.sv_tidx = rg.fuse->sv_tidx;
+        ga.sgbit = rg.fuse->sgbit;
+    }
     const uint64_t region_tiles = apply_region(ga, rg, all_tiles);
     ga.tile0 = std::min(rg.tile0, region_tiles);
     const uint64_t tiles = std::min(rg.count, region_tiles - ga.tile0);
     if (tiles == 0)
         return cudaSuccess;
     const int sms = rg.sms > 0 ? std::min(rg.sms, sm_count) : sm_count;
-    const uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * sms);
+    uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * sms);
+    if (rg.fuse)  // one flag per CTA (kFlagBytes)
+        grid = std::min<uint64_t>(grid, kFlagBytes / sizeof(unsigned long long));
     kern<<<static_cast<unsigned>(grid), NT, smem, stream>>>(st->amps, d_blob, step.blob_bytes,
                                                            step.nops, ga, rank_base, tiles);
     return cudaGetLastError();

@@ -541,12 +541,21 @@ extern "C" int qsv_state_alloc(qsv_ctx* ctx, int n_local, qsv_state** out, size_
     st->n_local = n_local;
     st->size = 1ull << n_local;
     const size_t b = sizeof(double2) * st->size;
-    cudaError_t e = qsv::dev_alloc(ctx, reinterpret_cast<void**>(&st->amps), b, 0);
+    // multi-rank shards carry the fused-swap flags after the amplitudes (peers reach them
+    // through the same mapping as the amplitudes)
+    const size_t extra = ctx->nranks > 1 ? qsv::kFlagBytes : 0;
+    cudaError_t e = qsv::dev_alloc(ctx, reinterpret_cast<void**>(&st->amps), b + extra, 0);
     if (e != cudaSuccess) {
         delete st;
         set_error("qsv_state_alloc: cudaMalloc of " + std::to_string(b) + " bytes failed: " +
                   cudaGetErrorString(e));
         return QSV_E_NOMEM;
+    }
+    if (extra && (e = cudaMemset(st->amps + st->size, 0, extra)) != cudaSuccess) {
+        qsv::dev_free(ctx, st->amps, 0);
+        delete st;
+        set_error(std::string("qsv_state_alloc: flag init: ") + cudaGetErrorString(e));
+        return QSV_E_CUDA;
     }
     if (bytes)
         *bytes = b;
@@ -1577,6 +1586,24 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
             continue;
         }
         const int v = s.desc.swap_local, b = s.desc.chunk_log2;
+        // BBOP: the swap fused into the next pass (the pass streams the peer's half over
+        // NVLink in its own loads), when P2P is up and the pass geometry allows it
+        if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 1) != 0 && i + 1 < prog->steps.size() &&
+            prog->steps[i + 1].desc.kind == QSV_STEP_PASS &&
+            (prog->jit_of_step.empty() || prog->jit_of_step[i + 1] < 0 ||
+             prog->jit_kernels[prog->jit_of_step[i + 1]].mt == 1)) {
+            qsv::FusedSwap fs;
+            const int rc = qsv::fused_swap_prepare(st, s.desc.swap_global, v, prog->steps[i + 1], &fs);
+            if (rc == QSV_OK) {
+                qsv::LaunchRange rg;
+                rg.fuse = &fs;
+                QSV_CUDA(launch_step(st, prog, i + 1, rank_base, rg, -2));
+                ++i;
+                continue;
+            }
+            if (rc != QSV_E_STATE)
+                return rc;
+        }
         if (p2p) {
             auto it = p2p_plan.find(i);
             if (it != p2p_plan.end() && it->second.post_end > i) {

@@ -99,6 +99,7 @@ struct qsv_state {
     bool peers_ready = false;
     std::vector<double2*> peer_amps;   // per rank, nullptr = not mapped
     std::vector<char> peer_ipc;        // 1 = opened with cudaIpcOpenMemHandle (close on free)
+    uint64_t fused_epoch = 0;          // fused swaps run on this buffer (flag epochs)
 };
 
 namespace qsv {
@@ -127,8 +128,18 @@ struct qsv_program {
 
 namespace qsv {
 void set_error(const std::string& msg);
+// A qubit swap fused into the pass that follows it (GeomArg::peer and friends).
+struct FusedSwap {
+    const double2* peer = nullptr;
+    unsigned long long* flag_mine = nullptr;
+    unsigned long long* flag_peer = nullptr;
+    uint64_t epoch = 0;
+    int sv = 0, sv_tile = 0, sv_tidx = 0;
+    uint32_t sgbit = 0;
+};
 // Tile range and SM budget of one pass launch (default: every tile, every SM).
 struct LaunchRange {
+    const FusedSwap* fuse = nullptr;  // the pass runs with a swap fused into its loads
     uint64_t tile0 = 0;
     uint64_t count = ~0ull;  // clipped to the pass's tile count
     int sms = 0;             // 0: all SMs; else persistent grid over this many SMs
@@ -163,6 +174,13 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf,
 // Collective on first use: maps the peers' shards; true when swap g will use NVLink P2P.
 bool p2p_swap_ready(qsv_state* st, int g);
 void join_swap(qsv_ctx* ctx);
+// Fused swap (g <-> v) into the pass `step` that follows it: maps the peers (collective on
+// first use), orders the compute stream after a pair barrier with the peer (both shards
+// final) and fills `out`.  QSV_E_STATE when P2P is unavailable or the pass geometry does
+// not allow it (v in the pass's contiguous low run): run a plain swap instead.
+int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out);
+// Fused-swap flags (one per CTA) live after the 2^l amplitudes of a state buffer.
+constexpr size_t kFlagBytes = 4096 * sizeof(unsigned long long);
 // Waits for `stream` on a multi-rank context without hanging on a dead peer: polls
 // the stream, the context's abort flag and ncclCommGetAsyncError, and aborts the
 // communicator (ncclCommAbort) after QSV_COLL_TIMEOUT_S seconds (default 900).

@@ -274,6 +274,60 @@ bool p2p_swap_ready(qsv_state* st, int g) {
     return st->peer_amps.size() == static_cast<size_t>(ctx->nranks) && peer < ctx->nranks && st->peer_amps[peer];
 }
 
+int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out) {
+    qsv_ctx* ctx = st->ctx;
+    const int l = st->n_local;
+    if (int rc = check_aborted(ctx, "qsv_swap (fused)"); rc != QSV_OK)
+        return rc;
+    if (!p2p_mode() || ctx->nranks < 2 || ctx->comm == nullptr || g < l || v < 0 || v >= l)
+        return QSV_E_STATE;
+    // geometry: v must not sit in the pass's contiguous low run (a run has one source)
+    const PassGeom& pg = step.geom;
+    if (v < pg.L)
+        return QSV_E_STATE;
+    int sv_tile = 0, below = 0;
+    for (int i = 0; i < pg.nhigh; ++i) {
+        if (pg.high[i] == v)
+            sv_tile = 1;
+        else if (pg.high[i] < v)
+            ++below;
+    }
+    if (!st->peers_ready) {
+        const int rc = exchange_peers(st);  // collective: every rank reaches its first swap
+        if (rc != QSV_OK)
+            return rc;
+    }
+    const int peer = ctx->rank ^ (1 << (g - l));
+    if (st->peer_amps.size() != static_cast<size_t>(ctx->nranks) || !st->peer_amps[peer])
+        return QSV_E_STATE;  // symmetric on one box: every rank takes the plain path
+    if (!ctx->d_sync) {
+        const cudaError_t e = dev_alloc(ctx, reinterpret_cast<void**>(&ctx->d_sync), 2 * sizeof(double), 3);
+        if (e != cudaSuccess)
+            return fail_cuda("qsv_swap: sync token cudaMalloc", e);
+        cudaMemset(ctx->d_sync, 0, 2 * sizeof(double));
+    }
+    // both shards are final before either side reads the other's
+    cudaEventRecord(ctx->ev_a, ctx->stream);
+    cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0);
+    const int tb = trace_open(ctx, QSV_TRACE_BARRIER, -2, 1, ctx->comm_stream);
+    const ncclResult_t r = pair_barrier(ctx, peer);
+    trace_close(ctx, tb, ctx->comm_stream);
+    if (r != ncclSuccess)
+        return fail_nccl("qsv_swap (fused): barrier", r);
+    cudaEventRecord(ctx->ev_b, ctx->comm_stream);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
+    out->peer = st->peer_amps[peer];
+    out->flag_mine = reinterpret_cast<unsigned long long*>(st->amps + st->size);
+    out->flag_peer = reinterpret_cast<unsigned long long*>(st->peer_amps[peer] + st->size);
+    out->epoch = ++st->fused_epoch;
+    out->sv = v;
+    out->sv_tile = sv_tile;
+    out->sv_tidx = v - pg.L - below;  // v's position among the tile-index (non-tile) bits
+    out->sgbit = static_cast<uint32_t>((ctx->rank >> (g - l)) & 1);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QSV_OK : fail_cuda("qsv_swap (fused)", e);
+}
+
 int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<cudaEvent_t>* chunk_done,
              uint64_t region_mask, const std::vector<cudaEvent_t>* pre_ready) {
     qsv_ctx* ctx = st->ctx;
