@@ -1587,8 +1587,11 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
         }
         const int v = s.desc.swap_local, b = s.desc.chunk_log2;
         // BBOP: the swap fused into the next pass (the pass streams the peer's half over
-        // NVLink in its own loads), when P2P is up and the pass geometry allows it
-        if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 1) != 0 && i + 1 < prog->steps.size() &&
+        // NVLink in its own loads), when P2P is up and the pass geometry allows it.  Opt-in
+        // (QSV_FUSE_SWAP=1): bitwise equal to swap + pass, but its remote TMA loads reach
+        // ~420 GB/s against the swap kernel's 695 (QFT-32 on 2 GPUs: 40.9 ms fused vs
+        // 24.7 + 15.0 ms), and random-34 on 2 GPUs ran 4.5 s vs 2.8 s (profiles/r02_bbop.md)
+        if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 0) != 0 && i + 1 < prog->steps.size() &&
             prog->steps[i + 1].desc.kind == QSV_STEP_PASS &&
             (prog->jit_of_step.empty() || prog->jit_of_step[i + 1] < 0 ||
              prog->jit_kernels[prog->jit_of_step[i + 1]].mt == 1)) {

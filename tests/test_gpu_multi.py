@@ -196,6 +196,9 @@ def test_pipeline_trace_nccl_chunks(two, monkeypatch):
     engines = _engines_in_threads(c, pkg.PlanOptions(chunk_log2=20, nbuf=B), 2)
     try:
         def go(e):
+            e.set_basis(0)
+            e.run()  # warm: peer setup, staging allocation
+            e.sync()
             e.trace_enable(True)
             e.set_basis(0)
             e.run()
@@ -247,7 +250,7 @@ def test_pipeline_trace_p2p(two):
         for e in engines:
             e.close()
     sw = [r for r in tr if r["kind"] == "swap"]
-    bars = [r for r in tr if r["kind"] == "barrier"]
+    bars = [r for r in tr if r["kind"] == "barrier" and r["chunk"] == -1]
     passes = [r for r in tr if r["kind"] == "pass"]
     assert sw and len(bars) == 2 * len(sw) and passes
     for k in sw:
@@ -320,7 +323,8 @@ def test_fused_swap_four_gpus(monkeypatch):
 
 
 @pytest.mark.timeout(600)
-def test_fused_swap_in_trace(two):
+def test_fused_swap_in_trace(two, monkeypatch):
+    monkeypatch.setenv("QSV_FUSE_SWAP", "1")
     c = pkg.Circuit.generate("qft:24")
     engines = _engines_in_threads(c, pkg.PlanOptions(), 2)
     try:
