@@ -54,3 +54,35 @@ def test_cli_report_json_csv(tmp_path):
     row = next(csv.DictReader(io.StringIO(out.read_text())))
     assert float(row["max_deviation"]) < 1e-10
     assert int(row["passes"]) >= 1 and float(row["gates_per_s"]) > 0
+
+
+def test_cli_ablate_verify_usage():
+    r = run("ablate")
+    assert r.returncode == 2 and "--gen" in r.stderr
+    r = run("frobnicate")
+    assert r.returncode == 2 and "ablate" in r.stderr
+
+
+@pytest.mark.gpu
+def test_cli_ablate_grid():
+    """cli_ablate: 2 sizes x {fusion} x {stagger} = 8 reports, speedups
+    against the all-off cell, and fusion never increases the op count."""
+    r = run("ablate", "--gen", "hea:14:3:1", "--sizes", "12,14", "--repeat", "1")
+    assert r.returncode == 0, r.stderr
+    rows = json.loads(r.stdout)
+    assert len(rows) == 8
+    for n in (12, 14):
+        cells = {x["cell"]: x for x in rows if x["qubits"] == n}
+        assert len(cells) == 4 and cells["fusion=off,stagger=off"]["speedup_vs_all_off"] == 1.0
+        assert cells["fusion=on,stagger=on"]["ops_final"] <= cells["fusion=off,stagger=on"]["ops_final"]
+        assert all(c["max_deviation"] < 1e-12 for c in cells.values())
+
+
+@pytest.mark.gpu
+def test_cli_verify_suite():
+    """cli_verify_suite: every criterion passes, each with its runtime."""
+    r = run("verify", "--quick")
+    assert r.returncode == 0, r.stdout + r.stderr
+    rows = list(csv.DictReader(io.StringIO(r.stdout.split("verify:")[0])))
+    assert len(rows) >= 8 and all(x["status"] == "pass" for x in rows)
+    assert all(float(x["seconds"]) >= 0 for x in rows)
