@@ -158,7 +158,161 @@ int jit_mt(int K) {
 // `mt` > 1: the CTA barrier of an op whose application depends on the tile (out-of-tile
 // controls) is hoisted out of the condition so every tile group meets it; ops with
 // internal CTA barriers under such a condition make the pass unsuitable (mt_ok = false).
-std::string gen_ops(const Step& s, const unsigned char* blob, int& minb, int mt = 1, bool* mt_ok = nullptr) {
+// Class-mode body of a register block (and the diagonal ops / relabel it absorbs): no
+// pass-specific constant appears in the text, so passes that differ only in qubit
+// positions, tables or blob offsets share one kernel.  Returns the index of the last op
+// it consumed.
+// (kind, a, b) primitive variants of the program's register blocks (class mode: the rolled
+// primitive switch carries exactly these, identical in every kernel of the program)
+thread_local const std::vector<int>* t_variants = nullptr;
+
+int gen_rblock_class(std::ostringstream& o, const Step& s, const unsigned char* blob, int i) {
+    const int K = s.geom.K;
+    const int NT = threads_for_k(K);
+    const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
+    const TileOp& op = ops[i];
+    const int KB = op.k, NV = 1 << KB;
+    auto ref = [](int j) {
+        return "(*reinterpret_cast<const qsv::TileOp*>(blob + " + std::to_string(j * sizeof(TileOp)) + "))";
+    };
+    std::ostringstream pre, epib;
+    int last = i;
+    if (op.xctrl == 0 && op.tctrl == 0 && !std::getenv("QSV_JIT_NO_EPI")) {
+        for (int j = i + 1; j < s.nops; ++j) {
+            const TileOp& d = ops[j];
+            if (d.kind != QSV_OP_DIAG && d.kind != QSV_OP_PHASEPROD && d.kind != QSV_OP_PARPHASE)
+                break;
+            const std::string J = std::to_string(j), D = "d" + J;
+            pre << "  const qsv::TileOp& " << D << " = " << ref(j) << ";\n";
+            std::string guard;
+            if (d.xctrl) {
+                pre << "  const bool on" << J << " = (full_base & " << D << ".xctrl) == " << D << ".xctrl;\n";
+                guard = "on" + J;
+            }
+            if (d.tctrl)
+                guard += std::string(guard.empty() ? "" : " && ") + "((idx & " + D + ".tctrl) == " + D + ".tctrl)";
+            std::string stmt;
+            if (d.kind == QSV_OP_DIAG) {
+                pre << "  const double2* g" << J << " = reinterpret_cast<const double2*>(blob + " << D << ".mat_byte);\n"
+                    << "  const uint32_t e" << J << " = qsv::diag_ext(" << D << ", full_base);\n";
+                if (d.nin == 0) {
+                    pre << "  const double2 c" << J << " = g" << J << "[e" << J << "];\n";
+                    stmt = "a = qsv::cmul(c" + J + ", a);";
+                } else if (d.nin == 1) {
+                    pre << "  const double2 c" << J << "a = g" << J << "[e" << J << "], c" << J << "b = g" << J << "[e" << J
+                        << " | 1u];\n  const int p" << J << " = __ffs(" << D << ".tmask) - 1;\n";
+                    stmt = "a = qsv::cmul(((idx >> p" + J + ") & 1u) ? c" + J + "b : c" + J + "a, a);";
+                } else {
+                    pre << "  const unsigned char* t" << J << " = blob + " << D << ".ptab_byte;\n";
+                    stmt = "a = qsv::cmul(g" + J + "[e" + J + " | t" + J + "[idx & 31u] | t" + J + "[32u + (idx >> 5)]], a);";
+                }
+            } else if (d.kind == QSV_OP_PHASEPROD) {
+                pre << "  const double2* g" << J << " = reinterpret_cast<const double2*>(blob + " << D << ".mat_byte);\n"
+                    << "  const double2 c" << J << " = qsv::pp_const(" << D << ", blob, full_base);\n";
+                stmt = "a = qsv::cmul(qsv::cmul(c" + J + ", qsv::cmul(g" + J + "[1u + (idx & 31u)], g" + J +
+                       "[33u + (idx >> 5)])), a);";
+            } else {
+                pre << "  double2 c" << J << "a, c" << J << "b;\n  qsv::par_consts(" << D << ", blob, full_base, c" << J
+                    << "a, c" << J << "b);\n";
+                stmt = "a = qsv::cmul((__popc(idx & " + D + ".tmask) & 1) ? c" + J + "b : c" + J + "a, a);";
+            }
+            for (int jm = 0; jm < NV; ++jm)
+                epib << "    { double2& a = v[" << jm << "]; const uint32_t idx = base ^ (" << ((jm & 1) ? "m0" : "0u")
+                     << " | " << ((jm & 2) ? "m1" : "0u") << " | " << ((jm & 4) ? "m2" : "0u") << " | "
+                     << ((jm & 8) ? "m3" : "0u") << "); (void)idx; " << (guard.empty() ? "" : "if (" + guard + ") ")
+                     << stmt << " }\n";
+            last = j;
+        }
+    }
+    const bool fold = last + 1 == s.nops - 1 && ops[last + 1].kind == QSV_OP_RELABEL && op.xctrl == 0 &&
+                      op.tctrl == 0 && (1 << (K - __builtin_popcount(op.fmask))) == NT &&
+                      env_int("QSV_JIT_FOLD_RELABEL", 1, 0, 1);
+    uint32_t rot = 0;
+    for (int l = 0; l < 8; ++l)
+        rot |= (op.rot_tab >> (4 * l)) & 15u;
+    o << pre.str();
+    o << "  const qsv::DevPrim* prs" << i << " = reinterpret_cast<const qsv::DevPrim*>(blob + " << ref(i) << ".prim_byte);\n";
+    o << "  qsv::jit_rblock_rt<" << K << ", " << NT << ", " << KB << (fold ? ", true" : ", false") << ">(tile, " << ref(i)
+      << ", [&](double2 (&v)[" << NV << "], uint32_t& r) {\n    (void)r;\n";
+    const DevPrim* pr = reinterpret_cast<const DevPrim*>(blob + op.prim_byte);
+    if (env_int("QSV_JIT_CLASS_ROLL", 1, 0, 1)) {
+        // rolled: one loop over the block's primitive records, a switch over every
+        // (kind, a, b) variant of a KB-qubit block; the rotation is applied at run time
+        o << "#pragma unroll 1\n    for (int p = 0; p < " << ref(i) << ".nprim; ++p) {\n"
+          << "      const qsv::DevPrim q = prs" << i << "[p];\n"
+          << "      const double2* m = reinterpret_cast<const double2*>(blob + q.data_byte); (void)m;\n"
+          << "      switch ((q.kind << 4) | (q.a << 2) | q.b) {\n";
+        auto want = [&](int key) {
+            return !t_variants || std::find(t_variants->begin(), t_variants->end(), key) != t_variants->end();
+        };
+        for (int a = 0; a < KB; ++a) {
+            const char* u1[3] = {"rb_u1", "rb_u1r", "rb_u1i"};
+            const int u1k[3] = {QSV_PRIM_U1, QSV_PRIM_U1R, QSV_PRIM_U1I};
+            for (int t = 0; t < 3; ++t)
+                if (want((u1k[t] << 4) | (a << 2)))
+                    o << "      case " << ((u1k[t] << 4) | (a << 2)) << ": qsv::" << u1[t] << "<" << NV << ", " << a
+                      << ">(v, m + 4u * ((r >> " << a << ") & 1u)); break;\n";
+            for (int b = 0; b < KB; ++b) {
+                if (b == a)
+                    continue;
+                if (want((QSV_PRIM_CX << 4) | (a << 2) | b))
+                    o << "      case " << ((QSV_PRIM_CX << 4) | (a << 2) | b) << ": qsv::rb_cx_plain<" << NV << ", "
+                      << a << ", " << b << ">(v); r ^= ((r >> " << a << ") & 1u) << " << b << "; break;\n";
+                if (b > a && want((QSV_PRIM_U2 << 4) | (a << 2) | b))
+                    o << "      case " << ((QSV_PRIM_U2 << 4) | (a << 2) | b) << ": qsv::rb_u2<" << NV << ", " << a
+                      << ", " << b << ">(v, m + 16u * (((r >> " << a << ") & 1u) | (((r >> " << b
+                      << ") & 1u) << 1))); break;\n";
+            }
+        }
+        if (want((QSV_PRIM_DIAG16 << 4) | (3 << 2) | 3))
+            o << "      case " << ((QSV_PRIM_DIAG16 << 4) | (3 << 2) | 3) << ": qsv::rb_diag<" << NV
+              << ">(v, m, r); break;\n";
+        o << "      default: break;\n      }\n    }\n";
+    } else
+    for (int p = 0; p < op.nprim; ++p) {
+        const DevPrim& q = pr[p];
+        const std::string mat = "reinterpret_cast<const double2*>(blob + prs" + std::to_string(i) + "[" +
+                                std::to_string(p) + "].data_byte)";
+        const bool ra = (rot >> q.a) & 1u, rb = (rot >> q.b) & 1u;
+        switch (q.kind) {
+        case QSV_PRIM_U1:
+        case QSV_PRIM_U1R:
+        case QSV_PRIM_U1I: {
+            const char* fn = q.kind == QSV_PRIM_U1 ? "rb_u1" : (q.kind == QSV_PRIM_U1R ? "rb_u1r" : "rb_u1i");
+            o << "    qsv::" << fn << "<" << NV << ", " << int(q.a) << ">(v, " << mat;
+            if (ra)
+                o << " + 4u * ((r >> " << int(q.a) << ") & 1u)";
+            o << ");\n";
+            break;
+        }
+        case QSV_PRIM_U2:
+            o << "    qsv::rb_u2<" << NV << ", " << int(q.a) << ", " << int(q.b) << ">(v, " << mat;
+            if (ra || rb)
+                o << " + 16u * (((r >> " << int(q.a) << ") & 1u) | (((r >> " << int(q.b) << ") & 1u) << 1))";
+            o << ");\n";
+            break;
+        case QSV_PRIM_CX:
+            o << "    qsv::rb_cx_plain<" << NV << ", " << int(q.a) << ", " << int(q.b) << ">(v);\n";
+            if (ra) {
+                o << "    r ^= ((r >> " << int(q.a) << ") & 1u) << " << int(q.b) << ";\n";
+                rot |= 1u << q.b;
+            }
+            break;
+        default:
+            o << "    qsv::rb_diag<" << NV << ">(v, " << mat << ", " << (rot ? "r" : "0u") << ");\n";
+            break;
+        }
+    }
+    o << "  }, [&](double2 (&v)[" << NV << "], uint32_t base, uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3) {\n"
+      << "    (void)v; (void)base; (void)m0; (void)m1; (void)m2; (void)m3;\n" << epib.str() << "  }";
+    if (fold)
+        o << ", &" << ref(last + 1);
+    o << ");\n";
+    return fold ? last + 1 : last;
+}
+
+std::string gen_ops(const Step& s, const unsigned char* blob, int& minb, int mt = 1, bool* mt_ok = nullptr,
+                    bool class_mode = false) {
     const int K = s.geom.K;
     const int NT = threads_for_k(K);
     const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
@@ -179,7 +333,9 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb, int mt 
             o << "  __syncthreads();\n";
             o << "  if ((full_base & " << u64(op.xctrl) << ") == " << u64(op.xctrl) << ") {\n";
         } else {
-            if (op.xctrl)
+            if (op.xctrl && class_mode)
+                o << "  if ((full_base & " << opref << ".xctrl) == " << opref << ".xctrl) {\n";
+            else if (op.xctrl)
                 o << "  if ((full_base & " << u64(op.xctrl) << ") == " << u64(op.xctrl) << ") {\n";
             o << "  __syncthreads();\n";
         }
@@ -211,6 +367,10 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb, int mt 
             o << "  qsv::xperm_op<" << K << ", " << NT << ">(tile, " << opref << ");\n";
             break;
         case QSV_OP_RBLOCK: {
+            if (class_mode && !split_blocks()) {
+                i = gen_rblock_class(o, s, blob, i);
+                break;
+            }
             // Diagonal ops right after a whole-tile register block ride along as a
             // per-amplitude epilogue: no extra SMEM sweep or barrier for them.
             std::ostringstream pre, epi, epib;
@@ -573,6 +733,10 @@ bool compile_unit(const std::string& src, std::vector<char>& cubin, std::string&
         std::snprintf(name, sizeof(name), "/qsv_%016llx.cu", static_cast<unsigned long long>(fnv1a(src)));
         std::ofstream(std::string(dump) + name) << src;
     }
+    if (std::getenv("QSV_JIT_DRYRUN")) {  // diagnostics: count the kernels without compiling
+        cubin.assign(1, 0);
+        return true;
+    }
     const std::string dir = cache_dir();
     const std::string path = unit_cache_path(src);
     if (use_cache) {
@@ -659,8 +823,50 @@ struct JitPlan {
 size_t jit_tile_smem(int K, int mt) { return sizeof(double2) * static_cast<size_t>(mt) * tile_nbuf() * (size_t{1} << K); }
 constexpr size_t kSmemPerCta = 227 * 1024 - 4096;  // opt-in limit minus the static arrays
 
+JitPlan plan_kernels_mode(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels,
+                          bool class_mode);
+
+// Fully specialised kernels (every structural quantity a constant) unless the program has
+// more than QSV_JIT_CLASS_MIN distinct passes: then structure classes (masks, slots, tables
+// and blob offsets read at run time, primitives through a rolled switch over the program's
+// variants) share kernels.  Opt-in: UCCSD-28 drops from 4436 to 132 kernels, but the
+// rolled bodies spill (48-164 B) and compile ~40x slower each, so NVRTC time does not
+// improve (69 s vs ~47 s cold on the same 8 host cores; profiles/r02_kernel_ab.md).
 JitPlan plan_kernels(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels) {
+    const int class_min = env_int("QSV_JIT_CLASS_MIN", 1 << 30, 0, 1 << 30);
+    JitPlan jp = plan_kernels_mode(steps, host_blobs, std::max(max_kernels, class_min + 1), false);
+    if (static_cast<int>(jp.bodies.size()) <= class_min && static_cast<int>(jp.bodies.size()) <= max_kernels)
+        return jp;
+    return plan_kernels_mode(steps, host_blobs, max_kernels, true);
+}
+
+JitPlan plan_kernels_mode(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels,
+                          bool class_mode) {
     JitPlan jp;
+    std::vector<int> variants;
+    if (class_mode) {
+        for (const Step& s : steps) {
+            if (s.desc.kind != QSV_STEP_PASS)
+                continue;
+            const unsigned char* blob = host_blobs + s.blob_off;
+            const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
+            for (int i = 0; i < s.nops; ++i) {
+                if (ops[i].kind != QSV_OP_RBLOCK)
+                    continue;
+                const DevPrim* pr = reinterpret_cast<const DevPrim*>(blob + ops[i].prim_byte);
+                for (int p = 0; p < ops[i].nprim; ++p) {
+                    const int key = (pr[p].kind << 4) | (pr[p].a << 2) | pr[p].b;
+                    if (std::find(variants.begin(), variants.end(), key) == variants.end())
+                        variants.push_back(key);
+                }
+            }
+        }
+        std::sort(variants.begin(), variants.end());
+    }
+    t_variants = class_mode ? &variants : nullptr;
+    struct Reset {
+        ~Reset() { t_variants = nullptr; }
+    } reset;
     std::map<std::string, int> uniq;
     jp.jit_of_step.assign(steps.size(), -1);
     for (size_t i = 0; i < steps.size(); ++i) {
@@ -670,10 +876,10 @@ JitPlan plan_kernels(const std::vector<Step>& steps, const unsigned char* host_b
         int minb = 3;
         int mt = jit_mt(s.geom.K);
         bool mt_ok = true;
-        std::string body = gen_ops(s, host_blobs + s.blob_off, minb, mt, &mt_ok);
+        std::string body = gen_ops(s, host_blobs + s.blob_off, minb, mt, &mt_ok, class_mode);
         if (mt > 1 && (!mt_ok || jit_tile_smem(s.geom.K, mt) + s.blob_bytes > kSmemPerCta)) {
             mt = 1;
-            body = gen_ops(s, host_blobs + s.blob_off, minb, 1, nullptr);
+            body = gen_ops(s, host_blobs + s.blob_off, minb, 1, nullptr, class_mode);
         }
         const std::string key = std::to_string(s.geom.K) + "|" + std::to_string(minb) + "|" + std::to_string(mt) +
                                 "|" + body;

@@ -1124,4 +1124,64 @@ __device__ __forceinline__ void jit_rblock(double2* tile, Body&& body, Epi&& epi
     }
 }
 
+// Structure-class form of jit_rblock (JIT class mode, programs with many distinct passes):
+// the enumeration masks, member slots and rotation table are read from the op record at
+// run time, so passes that differ only in qubit positions share one kernel.  `epib(v,
+// base, m0, m1, m2, m3)` sees the member masks; with PERM the pass relabel `rl` (a
+// RELABEL op record: destination of tile bit b in tpos[b] / xbit[b - 8]) is folded into
+// the stores.
+__device__ __forceinline__ uint32_t relabel_map(const TileOp& rl, int K, uint32_t x) {
+    uint32_t y = 0;
+    for (int b = 0; b < K; ++b)
+        y |= ((x >> b) & 1u) << (b < 8 ? rl.tpos[b] : rl.xbit[b - 8]);
+    return y;
+}
+
+template <int K, int NT, int KB, bool PERM = false, typename Body, typename EpiB>
+__device__ __forceinline__ void jit_rblock_rt(double2* tile, const TileOp& op, Body&& body, EpiB&& epib,
+                                              const TileOp* rl = nullptr) {
+    constexpr int NV = 1 << KB;
+    const int nfix = op.nfix;
+    const uint32_t F = op.fmask, tctrl = op.tctrl;
+    const uint32_t groups = 1u << (K - nfix);
+    if (groups < static_cast<uint32_t>(NT) && QSV_LTID >= groups)
+        return;
+    const uint32_t steps = groups >= static_cast<uint32_t>(NT) ? groups / NT : 1u;
+    const uint32_t dstep = deposit(NT, op.fixpos, nfix);
+    const uint32_t m0 = 1u << op.tpos[0], m1 = 1u << op.tpos[1], m2 = 1u << op.tpos[2],
+                   m3 = KB > 3 ? 1u << op.tpos[3] : 0u;
+    auto moff = [&](uint32_t j) {
+        return ((j & 1u) ? m0 : 0u) | ((j & 2u) ? m1 : 0u) | ((j & 4u) ? m2 : 0u) | ((j & 8u) ? m3 : 0u);
+    };
+    const uint32_t r0 = (op.rot_tab >> (4 * (QSV_LTID & 7))) & 15u;
+    const uint32_t offr = moff(r0);
+    uint32_t b = deposit(QSV_LTID, op.fixpos, nfix);
+#pragma unroll 1
+    for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t base_in = b | tctrl | offr;
+        double2 v[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j)
+            v[j] = tile[base_in ^ moff(static_cast<uint32_t>(j))];
+        uint32_t r = r0;
+        body(v, r);
+        const uint32_t base = b | tctrl | moff(r);
+        epib(v, base, m0, m1, m2, m3);
+        if constexpr (PERM) {
+            __syncthreads();  // every member has been read before any permuted store
+            const uint32_t mb = relabel_map(*rl, K, base);
+            const uint32_t q0 = relabel_map(*rl, K, m0), q1 = relabel_map(*rl, K, m1),
+                           q2 = relabel_map(*rl, K, m2), q3 = relabel_map(*rl, K, m3);
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+                tile[mb ^ (((j & 1) ? q0 : 0u) | ((j & 2) ? q1 : 0u) | ((j & 4) ? q2 : 0u) | ((j & 8) ? q3 : 0u))] = v[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < NV; ++j)
+                tile[base ^ moff(static_cast<uint32_t>(j))] = v[j];
+        }
+        b = next_group(b, F, dstep);
+    }
+}
+
 } // namespace qsv

@@ -50,3 +50,14 @@ def test_jit_kernels_compile(spec, kw):
     rc, nk = E.jit_check(steps, ops, prims, pool, c.n, c.n)
     assert rc == 0, pkg.load_qsv().qsv_last_error()
     assert nk >= 1
+
+
+@pytest.mark.skipif(not _nvrtc_present(), reason="libnvrtc not in this image")
+def test_class_mode_kernels_compile(monkeypatch):
+    """Structure-class kernels (QSV_JIT_CLASS_MIN): runtime masks, rolled primitive switch."""
+    monkeypatch.setenv("QSV_JIT_CLASS_MIN", "0")
+    c = pkg.Circuit.generate("uccsd:14:400:3")
+    steps, ops, prims, pool = E.export_plan(c, pkg.PlanOptions(relabel=2), c.n)
+    rc, nk = E.jit_check(steps, ops, prims, pool, c.n, c.n)
+    assert rc == 0, pkg.load_qsv().qsv_last_error()
+    assert 1 <= nk < len([s for s in steps if s.kind == 0])
