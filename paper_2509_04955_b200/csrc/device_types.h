@@ -113,6 +113,11 @@ struct GeomArg {
     uint64_t epoch;                 // flag value of iteration i: (epoch << 32) | (i + 1)
     int32_t sv, sv_tile, sv_tidx;   // sv_tidx (sv_tile = 0): tile-index bit of sv
     uint32_t sgbit;
+    // debug (QSV_DEBUG_POISON=1): every tile buffer run is filled with NaN before its
+    // TMA load is issued, so an op that reads SMEM the load has not yet written (a broken
+    // mbarrier / bulk-copy ordering) turns the result into NaN instead of a stale value
+    int32_t poison;
+    int32_t pad_;
 };
 
 // Largest per-pass blob (bytes of shared memory on top of the tile buffers).

@@ -1039,6 +1039,13 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
     ga.nhigh = s.geom.nhigh;
     for (int i = 0; i < s.geom.nhigh; ++i)
         ga.high[i] = s.geom.high[i];
+    {
+        static const int poison = [] {
+            const char* e = std::getenv("QSV_DEBUG_POISON");
+            return e && e[0] == '1' ? 1 : 0;
+        }();
+        ga.poison = poison;
+    }
     if (rg.fuse) {
         ga.peer = rg.fuse->peer;
         ga.flag_mine = rg.fuse->flag_mine;
@@ -1058,6 +1065,8 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
     const int sms = rg.sms > 0 ? std::min(rg.sms, st->ctx->sm_count) : st->ctx->sm_count;
     const uint64_t ctas_needed = (tiles + jk.mt - 1) / jk.mt;
     uint64_t grid = std::min<uint64_t>(ctas_needed, static_cast<uint64_t>(per_sm) * sms);
+    if (const char* g = std::getenv("QSV_DEBUG_GRID"))  // debug: fewer persistent CTAs, other tile order
+        grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, std::strtoull(g, nullptr, 10)));
     if (rg.fuse)  // one flag per CTA (kFlagBytes)
         grid = std::min<uint64_t>(grid, kFlagBytes / sizeof(unsigned long long));
     double2* psi = st->amps;

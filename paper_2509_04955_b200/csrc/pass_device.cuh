@@ -837,6 +837,16 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         if (lane == 0)
             mbar_expect_tx(&mbar[b], static_cast<uint32_t>(my_runs) * run_bytes);
         __syncwarp();
+        if (geom.poison) {  // debug: NaN in this warp's runs of the buffer, then the loads
+            const double nan = __longlong_as_double(0x7ff8dead00000000ll);
+            for (int k = 0; k < my_runs; ++k) {
+                double2* run = dst + ((warp + NW * k) << RL);
+                for (int e = lane; e < (1 << RL); e += 32)
+                    run[e] = make_double2(nan, nan);
+            }
+            fence_proxy_async();
+            __syncwarp();
+        }
         for (int k = lane; k < my_runs; k += 32) {
             const int j = warp + NW * k;
             const uint64_t idx = base + hi_off[j << m];

@@ -34,6 +34,7 @@
 #include "pass_device.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace qsv {
 
@@ -126,6 +127,13 @@ cudaError_t launch_variant(const qsv_state* st, const Step& step, const unsigned
     for (int i = 0; i < step.geom.nhigh; ++i)
         ga.high[i] = step.geom.high[i];
     const uint64_t all_tiles = st->size >> K;
+    {
+        static const int poison = [] {
+            const char* e = std::getenv("QSV_DEBUG_POISON");
+            return e && e[0] == '1' ? 1 : 0;
+        }();
+        ga.poison = poison;
+    }
     if (rg.fuse) {
         ga.peer = rg.fuse->peer;
         ga.flag_mine = rg.fuse->flag_mine;
@@ -143,6 +151,8 @@ cudaError_t launch_variant(const qsv_state* st, const Step& step, const unsigned
         return cudaSuccess;
     const int sms = rg.sms > 0 ? std::min(rg.sms, sm_count) : sm_count;
     uint64_t grid = std::min<uint64_t>(tiles, static_cast<uint64_t>(per_sm) * sms);
+    if (const char* g = std::getenv("QSV_DEBUG_GRID"))  // debug: fewer persistent CTAs, other tile order
+        grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, std::strtoull(g, nullptr, 10)));
     if (rg.fuse)  // one flag per CTA (kFlagBytes)
         grid = std::min<uint64_t>(grid, kFlagBytes / sizeof(unsigned long long));
     kern<<<static_cast<unsigned>(grid), NT, smem, stream>>>(st->amps, d_blob, step.blob_bytes,

@@ -289,3 +289,26 @@ def test_random30_full_size_vs_oracle():  # configs[1] at full size against the 
         worst = max(worst, e.max_abs_diff(ref[off:off + step], off))
     e.close()
     assert worst <= TOL
+
+
+def _sanitize_digests(env):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize.py")], capture_output=True, text=True,
+                       env={**os.environ, **env}, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return [ln for ln in r.stdout.splitlines() if ln.startswith("DIGEST")]
+
+
+def test_race_checks_poison_and_grid():
+    """Race checks without compute-sanitizer (closed on this pool): every kernel flavour gives
+    bitwise the same state with NaN-poisoned tile buffers before each TMA load (a read that
+    overtakes its load, or a store that still reads a reloaded buffer, would surface as NaN
+    or a different digest) and with 1 or 7 persistent CTAs instead of the full grid (other
+    tile order, pipeline phase and buffer reuse pattern)."""
+    base = _sanitize_digests({})
+    assert len(base) >= 6
+    for env in ({"QSV_DEBUG_POISON": "1"}, {"QSV_DEBUG_GRID": "1"}, {"QSV_DEBUG_GRID": "7", "QSV_DEBUG_POISON": "1"}):
+        assert _sanitize_digests(env) == base, env

@@ -1,7 +1,10 @@
-"""Small circuits through every pass-kernel flavour, for compute-sanitizer runs
-(racecheck / synccheck / memcheck): the NVRTC-specialised kernels, the interpreter,
-relabel passes and relabels folded into register-block stores, dense k<=5 ops,
-12-qubit tiles and the DMMA16 op.  Each result is checked against the CPU oracle.
+"""Small circuits through every pass-kernel flavour: the NVRTC-specialised kernels, the
+interpreter, relabel passes and relabels folded into register-block stores, dense k<=5
+ops and 12-qubit tiles.  Each result is checked against the CPU oracle and its bitwise
+digest printed, so runs under the debug switches (QSV_DEBUG_POISON=1: NaN-filled tile
+buffers before every TMA load; QSV_DEBUG_GRID=N: N persistent CTAs, another tile order
+and pipeline phase) can be compared bit for bit (tests/test_gpu_parity.py).  Also the
+compute-sanitizer driver where that tool is available:
   compute-sanitizer --tool racecheck python tools/sanitize.py
 """
 import os
@@ -33,9 +36,11 @@ def main():
         e.run()
         e.sync()
         got = e.download()
+        dig = e.digest()
         e.close()
         err = float(np.abs(got - O.run_local(c)).max())
         worst = max(worst, err)
+        print(f"DIGEST {spec} {sorted(kw.items())} {dig:016x}", flush=True)
         print(f"{spec} {kw} max-abs {err:.2e}", flush=True)
     assert worst <= 1e-10, worst
     print("sanitize cases ok", flush=True)
