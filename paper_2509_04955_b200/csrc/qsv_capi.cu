@@ -1607,6 +1607,33 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
             if (rc != QSV_E_STATE)
                 return rc;
         }
+        if (evs == nullptr && !overlap && env_int("QSV_MERGE_SWAPS", 1) != 0 && i + 1 < prog->steps.size() &&
+            prog->steps[i + 1].desc.kind == QSV_STEP_SWAP && qsv::p2p_swap_ready(st, s.desc.swap_global)) {
+            // consecutive swaps of distinct global and distinct local qubits: one all-to-all
+            int gs[3] = {s.desc.swap_global, 0, 0}, vs[3] = {v, 0, 0}, k = 1;
+            size_t j = i + 1;
+            while (k < 3 && j < prog->steps.size() && prog->steps[j].desc.kind == QSV_STEP_SWAP) {
+                const qsv_step_desc& d2 = prog->steps[j].desc;
+                bool disjoint = true;
+                for (int q = 0; q < k; ++q)
+                    disjoint = disjoint && d2.swap_global != gs[q] && d2.swap_local != vs[q];
+                if (!disjoint)
+                    break;
+                gs[k] = d2.swap_global;
+                vs[k] = d2.swap_local;
+                ++k;
+                ++j;
+            }
+            if (k >= 2) {
+                const int rc = qsv::run_multi_swap(st, gs, vs, k);
+                if (rc == QSV_OK) {
+                    i = j - 1;
+                    continue;
+                }
+                if (rc != QSV_E_STATE)
+                    return rc;
+            }
+        }
         if (p2p) {
             auto it = p2p_plan.find(i);
             if (it != p2p_plan.end() && it->second.post_end > i) {

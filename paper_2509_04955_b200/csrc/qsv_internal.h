@@ -179,6 +179,9 @@ void join_swap(qsv_ctx* ctx);
 // final) and fills `out`.  QSV_E_STATE when P2P is unavailable or the pass geometry does
 // not allow it (v in the pass's contiguous low run): run a plain swap instead.
 int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out);
+// k = 2 or 3 consecutive disjoint swaps (gs[i] <-> vs[i]) as one NVLink P2P all-to-all
+// among the 2^k ranks that differ in the g bits.  QSV_E_STATE when P2P is unavailable.
+int run_multi_swap(qsv_state* st, const int* gs, const int* vs, int k);
 // Fused-swap flags (one per CTA) live after the 2^l amplitudes of a state buffer.
 constexpr size_t kFlagBytes = 4096 * sizeof(unsigned long long);
 // Waits for `stream` on a multi-rank context without hanging on a dead peer: polls

@@ -20,6 +20,7 @@
 
 #include <unistd.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -272,6 +273,91 @@ bool p2p_swap_ready(qsv_state* st, int g) {
     const int l = st->n_local;
     const int peer = ctx->rank ^ (1 << (g - l));
     return st->peer_amps.size() == static_cast<size_t>(ctx->nranks) && peer < ctx->nranks && st->peer_amps[peer];
+}
+
+// Several consecutive qubit swaps (g_i <-> v_i, distinct g and distinct v) as one
+// all-to-all over NVLink P2P: the 2^k ranks that differ only in the g bits
+// exchange blocks pairwise — rank r's block with v bits = y goes to the rank whose g bits
+// are y, which sends back its block with v bits = r's g bits — so each GPU moves
+// (2^k - 1) / 2^k of its shard once instead of k / 2 of it k times.  Each pair block is
+// swapped in place by the region kernel, the lower rank taking the first half of the
+// pairs; grouped NCCL token send/recv with every partner bracket the exchange.
+int run_multi_swap(qsv_state* st, const int* gs, const int* vs, int k) {
+    qsv_ctx* ctx = st->ctx;
+    const int l = st->n_local;
+    if (int rc = check_aborted(ctx, "qsv_swap (multi)"); rc != QSV_OK)
+        return rc;
+    if (k < 2 || k > 3 || !p2p_mode() || ctx->nranks < (1 << k) || ctx->comm == nullptr)
+        return QSV_E_STATE;
+    if (!st->peers_ready) {
+        const int rc = exchange_peers(st);
+        if (rc != QSV_OK)
+            return rc;
+    }
+    uint32_t mybits = 0;
+    uint64_t gmask = 0;
+    for (int i = 0; i < k; ++i) {
+        mybits |= static_cast<uint32_t>((ctx->rank >> (gs[i] - l)) & 1) << i;
+        gmask |= 1ull << (gs[i] - l);
+    }
+    std::vector<int> partners;
+    for (uint32_t y = 0; y < (1u << k); ++y) {
+        if (y == mybits)
+            continue;
+        int r = ctx->rank & ~static_cast<int>(gmask);
+        for (int i = 0; i < k; ++i)
+            r |= static_cast<int>((y >> i) & 1u) << (gs[i] - l);
+        if (st->peer_amps.size() != static_cast<size_t>(ctx->nranks) || !st->peer_amps[r])
+            return QSV_E_STATE;
+        partners.push_back(r);
+    }
+    auto group_barrier = [&]() {
+        ncclResult_t r = ncclGroupStart();
+        for (int q : partners) {
+            if (r == ncclSuccess) r = ncclSend(ctx->d_sync, 1, ncclDouble, q, ctx->comm, ctx->comm_stream);
+            if (r == ncclSuccess) r = ncclRecv(ctx->d_sync + 1, 1, ncclDouble, q, ctx->comm, ctx->comm_stream);
+        }
+        const ncclResult_t r2 = ncclGroupEnd();
+        return r != ncclSuccess ? r : r2;
+    };
+    cudaEventRecord(ctx->ev_a, ctx->stream);
+    cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0);
+    int tb = trace_open(ctx, QSV_TRACE_BARRIER, -3, 1, ctx->comm_stream);
+    ncclResult_t r = group_barrier();  // every partner's earlier passes are done
+    trace_close(ctx, tb, ctx->comm_stream);
+    if (r != ncclSuccess)
+        return fail_nccl("qsv_swap (multi): barrier", r);
+    int pos[3];
+    for (int i = 0; i < k; ++i)
+        pos[i] = vs[i];
+    std::sort(pos, pos + k);
+    const uint64_t pairs = 1ull << (l - k);
+    for (size_t pi = 0; pi < partners.size(); ++pi) {
+        const int q = partners[pi];
+        uint32_t y = 0;
+        for (int i = 0; i < k; ++i)
+            y |= static_cast<uint32_t>((q >> (gs[i] - l)) & 1) << i;
+        uint64_t mine_v = 0, theirs_v = 0;
+        for (int i = 0; i < k; ++i) {
+            mine_v |= static_cast<uint64_t>((y >> i) & 1u) << vs[i];
+            theirs_v |= static_cast<uint64_t>((mybits >> i) & 1u) << vs[i];
+        }
+        const uint64_t half = pairs / 2;
+        const uint64_t begin = ctx->rank < q ? 0 : half;
+        const int tk = trace_open(ctx, QSV_TRACE_SWAP, -3, 1, ctx->comm_stream);
+        p2p_swap_region_kernel<<<ctx->sm_count * 4, 256, 0, ctx->comm_stream>>>(
+            st->amps, st->peer_amps[q], begin, half, pos[0], k > 1 ? pos[1] : 0, k > 2 ? pos[2] : 0, k, 0ull, mine_v,
+            theirs_v);
+        trace_close(ctx, tk, ctx->comm_stream);
+    }
+    tb = trace_open(ctx, QSV_TRACE_BARRIER, -3, 1, ctx->comm_stream);
+    r = group_barrier();  // every partner's writes into this shard are done
+    trace_close(ctx, tb, ctx->comm_stream);
+    if (r != ncclSuccess)
+        return fail_nccl("qsv_swap (multi): barrier", r);
+    join_swap(ctx);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? QSV_OK : fail_cuda("qsv_swap (multi): kernel", e);
 }
 
 int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out) {

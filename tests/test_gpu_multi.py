@@ -340,3 +340,19 @@ def test_fused_swap_in_trace(two, monkeypatch):
             e.close()
     fused = [r for r in tr if r["kind"] == "pass" and r["chunk"] == -2]
     assert fused, "no swap was fused into its pass"
+
+
+@pytest.mark.parametrize("spec", ["random:20:10:2", "qft:20", "hea:19:3:4", "random:22:12:2"])
+def test_merged_swaps_four_gpus(spec, monkeypatch):
+    """Consecutive disjoint qubit swaps run as one NVLink all-to-all among the 4 ranks
+    (each GPU moves 3/4 of its shard once instead of 1/2 twice): bitwise equal to the
+    pairwise swaps, and the oracle's state to 1e-10."""
+    if ngpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    c = pkg.Circuit.generate(spec)
+    monkeypatch.setenv("QSV_MERGE_SWAPS", "0")
+    pairwise, _ = run_dist(c, 2, 14, 2)
+    monkeypatch.setenv("QSV_MERGE_SWAPS", "1")
+    merged, _ = run_dist(c, 2, 14, 2)
+    assert np.array_equal(pairwise, merged)
+    assert np.abs(merged - O.run_local(c)).max() <= 1e-10
