@@ -258,9 +258,10 @@ int cmd_verify(std::map<std::string, std::string>& f) {
             v = {false, std::string("exception: ") + e.what()};
         }
         failed += v.pass ? 0 : 1;
-        std::string d = v.detail;
+        std::string d = v.detail, nm = name;
         std::replace(d.begin(), d.end(), ',', ';');
-        rows.push_back({{"criterion", name}, {"status", v.pass ? "pass" : "FAIL"}, {"seconds", std::to_string(secs(a, Clock::now()))},
+        std::replace(nm.begin(), nm.end(), ',', ';');
+        rows.push_back({{"criterion", nm}, {"status", v.pass ? "pass" : "FAIL"}, {"seconds", std::to_string(secs(a, Clock::now()))},
                         {"detail", d}});
     };
     qsim::DeviceContext ctx(0);
@@ -271,14 +272,17 @@ int cmd_verify(std::map<std::string, std::string>& f) {
         ctx.sync();
     };
     // #1 (device form): random mnemonic circuits n in [2, 10]: C C^dagger |0> = |0>, norm kept
-    crit("1 kernel correctness (mirror circuits, n 2..10)", [&] {
+    crit("1 kernel correctness (mirror circuits n 2..10)", [&] {
         double worst = 0.0;
         const int count = quick ? 40 : 200;
         for (int i = 0; i < count; ++i) {
             const int n = 2 + i % 9;
             const qsim::Circuit c = mirror(qsim::generate("random:" + std::to_string(n) + ":" + std::to_string(1 + i % 6) + ":" + std::to_string(100 + i)));
             qsim::DeviceState st(ctx, n);
-            run_state(c, qsim::PlanOptions{}, st, 0);
+            qsim::PlanOptions o;
+            o.jit = i % 4 == 0;  // every 4th through NVRTC kernels, the rest through the interpreter
+            o.tile_k = std::min(o.tile_k, n);
+            run_state(c, o, st, 0);
             qsim::Amp a0;
             st.download(&a0, 0, 1);
             worst = std::max({worst, std::abs(a0 - qsim::Amp(1.0, 0.0)), std::abs(st.norm_sq() - 1.0)});
