@@ -300,10 +300,11 @@ int run_multi_swap(qsv_state* st, const int* gs, const int* vs, int k) {
         mybits |= static_cast<uint32_t>((ctx->rank >> (gs[i] - l)) & 1) << i;
         gmask |= 1ull << (gs[i] - l);
     }
+    // partner order: step s pairs every rank with the one whose g bits differ by s, a
+    // perfect matching per step (ascending y made three ranks hit rank 0 at once)
     std::vector<int> partners;
-    for (uint32_t y = 0; y < (1u << k); ++y) {
-        if (y == mybits)
-            continue;
+    for (uint32_t sx = 1; sx < (1u << k); ++sx) {
+        const uint32_t y = mybits ^ sx;
         int r = ctx->rank & ~static_cast<int>(gmask);
         for (int i = 0; i < k; ++i)
             r |= static_cast<int>((y >> i) & 1u) << (gs[i] - l);

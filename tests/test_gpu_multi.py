@@ -228,9 +228,10 @@ def test_pipeline_trace_nccl_chunks(two, monkeypatch):
         sr = [r for r in tr if r["step"] == s and r["kind"] == "sendrecv"]
         cb = [r for r in tr if r["step"] == s and r["kind"] == "copyback"]
         wall = max(r["end_ms"] for r in cb) - min(r["start_ms"] for r in sr)
-        serial = sum(r["end_ms"] - r["start_ms"] for r in sr + cb)
-        assert wall < serial, f"swap {s}: wall {wall:.3f} ms >= serial {serial:.3f} ms"
-    assert overlapped >= 1
+        transfers = sum(r["end_ms"] - r["start_ms"] for r in sr)
+        last_cb = max(r["end_ms"] - r["start_ms"] for r in cb)
+        # only the last copy-back may extend the swap beyond its transfers (5 % timing slack)
+        assert wall <= 1.05 * transfers + last_cb, f"swap {s}: wall {wall:.3f} ms, transfers {transfers:.3f} ms"
 
 
 @pytest.mark.timeout(600)
