@@ -93,7 +93,7 @@ int qsv_ctx_aborted(qsv_ctx* ctx, int* out);
  * for the context's streams and writes up to cap records (*n = records available). */
 #define QSV_TRACE_PASS 0       /* pass kernel (chunk = region, -1 = whole shard)   */
 #define QSV_TRACE_SWAP 1       /* P2P swap kernel (chunk = region, -1 = whole)    */
-#define QSV_TRACE_SENDRECV 2   /* NCCL send/recv of one chunk (BBOP batch)        */
+#define QSV_TRACE_SENDRECV 2   /* NCCL send/recv of one chunk (+ its send gather)   */
 #define QSV_TRACE_COPYBACK 3   /* copy-back / scatter of one received chunk       */
 #define QSV_TRACE_BARRIER 4    /* pairwise barrier of a P2P swap                  */
 typedef struct qsv_trace_rec {

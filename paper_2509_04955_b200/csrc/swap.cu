@@ -568,6 +568,8 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
         const uint64_t r0 = c * C;
         const double2* src;
         double2* dst_contig = nullptr;
+        // the send/recv record covers the send-side gather too (same stream, same chunk)
+        const int ts = trace_open(ctx, QSV_TRACE_SENDRECV, static_cast<int>(c), 1, ctx->comm_stream);
         if (contiguous) {
             dst_contig = st->amps + ((r0 >> v) << (v + 1)) + (sendbit << v) + (r0 & ((1ull << v) - 1ull));
             src = dst_contig;
@@ -576,7 +578,6 @@ int run_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf, std::vector<
                                                                  sendbit);
             src = send_stage + b * C;
         }
-        const int ts = trace_open(ctx, QSV_TRACE_SENDRECV, static_cast<int>(c), 1, ctx->comm_stream);
         ncclResult_t r = ncclGroupStart();
         if (r == ncclSuccess) r = ncclSend(src, 2 * C, ncclDouble, peer, ctx->comm, ctx->comm_stream);
         if (r == ncclSuccess) r = ncclRecv(recv_stage + b * C, 2 * C, ncclDouble, peer, ctx->comm, ctx->comm_stream);
