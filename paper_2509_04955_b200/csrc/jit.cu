@@ -600,10 +600,37 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb, int mt 
             // host stores every U1/U2 matrix in all rotation variants.
             uint32_t rot = rot_any;
             const bool dyn_rot = env_int("QSV_JIT_DYNROT", 1, 0, 1) != 0;
+            // Matrices of primitives whose slots are not rotated are emitted as literal
+            // constants: the compiler folds them into constant-bank DFMA operands, saving the
+            // SMEM loads and the registers that held them (QSV_JIT_LITERALS=0: from the blob)
+            const bool literals = env_int("QSV_JIT_LITERALS", 1, 0, 1) != 0;
+            int nlit = 0;
+            auto lit = [&](const DevPrim& q, int n) {  // declares a local constant array, returns its name
+                const double* d = reinterpret_cast<const double*>(blob + q.data_byte);
+                const std::string name = "cm" + std::to_string(nlit++);
+                std::ostringstream t;
+                t << "    const double2 " << name << "[" << n << "] = {";
+                char buf[96];
+                for (int e = 0; e < n; ++e) {
+                    std::snprintf(buf, sizeof(buf), "%s{%a, %a}", e ? ", " : "", d[2 * e], d[2 * e + 1]);
+                    t << buf;
+                }
+                t << "};\n";
+                o << t.str();
+                return name;
+            };
             for (int p = 0; p < op.nprim; ++p) {
                 const DevPrim& q = pr[p];
-                const std::string mat = "reinterpret_cast<const double2*>(blob + " + std::to_string(q.data_byte) + ")";
+                std::string mat = "reinterpret_cast<const double2*>(blob + " + std::to_string(q.data_byte) + ")";
                 const bool ra = (rot >> q.a) & 1u, rb = (rot >> q.b) & 1u;
+                if (literals) {
+                    if ((q.kind == QSV_PRIM_U1 || q.kind == QSV_PRIM_U1R || q.kind == QSV_PRIM_U1I) && !ra)
+                        mat = lit(q, 4);
+                    else if (q.kind == QSV_PRIM_U2 && !ra && !rb)
+                        mat = lit(q, 16);
+                    else if (q.kind == QSV_PRIM_DIAG16 && rot == 0)
+                        mat = lit(q, NV);
+                }
                 if (q.kind == QSV_PRIM_CX && ra && dyn_rot) {
                     o << "    qsv::rb_cx_plain<" << NV << ", " << int(q.a) << ", " << int(q.b) << ">(v);\n";
                     o << "    r ^= ((r >> " << int(q.a) << ") & 1u) << " << int(q.b) << ";\n";
