@@ -15,6 +15,10 @@ typedef unsigned long long uint64_t;
 #include <cstdint>
 #endif
 
+#if !defined(__CUDACC__) && !defined(__CUDACC_RTC__) && !defined(__align__)
+#define __align__(n) alignas(n)
+#endif
+
 #ifndef QSV_H
 // values mirror include/qsv.h (static_assert-checked in qsv_internal.h)
 #define QSV_MAX_DENSE_K 5
@@ -117,7 +121,23 @@ struct GeomArg {
     // TMA load is issued, so an op that reads SMEM the load has not yet written (a broken
     // mbarrier / bulk-copy ordering) turns the result into NaN instead of a stale value
     int32_t poison;
+    // Tensor-map tile copies (JIT kernels): with tm_rank > 0 the tile moves as 2^tm_nx
+    // cp.async.bulk.tensor copies of a rank-tm_rank box instead of one bulk copy per
+    // contiguous run.  Dim d covers amplitude-index bits [tm_s[d], tm_s[d + 1]) (the last
+    // up to n_local); its box is the tile run starting at tm_s[d].  The tile bits above
+    // the last boxed run (tm_x[0..tm_nx)) are iterated, one copy per value.
+    int32_t tm_rank;
+    int32_t tm_s[5];
+    int32_t tm_nx;
+    int32_t tm_x[QSV_MAX_HIGH];
+    uint32_t tm_box_amps;
     int32_t pad_;
+};
+
+// The 128-byte CUDA tensor map (CUtensorMap), passed to the specialised kernels as a
+// __grid_constant__ parameter (opaque here).
+struct __align__(64) TmaDesc {
+    unsigned long long v[16];
 };
 
 // Largest per-pass blob (bytes of shared memory on top of the tile buffers).

@@ -91,6 +91,9 @@ struct Driver {
     CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                        CUstream, void**, void**) = nullptr;
     CUresult (*unload)(CUmodule) = nullptr;
+    CUresult (*encode_tiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill) = nullptr;
 };
 
 template <typename F>
@@ -111,6 +114,8 @@ const Driver& driver() {
                entry("cuFuncSetAttribute", d.set_attr) &&
                entry("cuOccupancyMaxActiveBlocksPerMultiprocessor", d.occupancy) &&
                entry("cuLaunchKernel", d.launch) && entry("cuModuleUnload", d.unload);
+        if (!entry("cuTensorMapEncodeTiled", d.encode_tiled))
+            d.encode_tiled = nullptr;  // tensor-map tile copies off
     });
     return d;
 }
@@ -708,13 +713,14 @@ std::string kernel_source(const std::string& name, int K, int minb, const std::s
     const int NT = threads_for_k(K);
     o << "extern \"C\" __global__ void __launch_bounds__(" << NT * mt << ", " << (mt > 1 ? 1 : minb) << ") " << name
       << "(double2* __restrict__ psi, const unsigned char* __restrict__ gblob, uint32_t blob_bytes,\n"
-      << "    const __grid_constant__ qsv::GeomArg geom, uint64_t rank_base, uint64_t ntiles) {\n"
+      << "    const __grid_constant__ qsv::GeomArg geom, uint64_t rank_base, uint64_t ntiles,\n"
+      << "    const __grid_constant__ qsv::TmaDesc tmap) {\n"
       << "  qsv::pass_pipeline<" << K << ", " << NT << ", " << tile_nbuf() << ", " << tile_pd() << ", "
       << (env_int("QSV_TMA_SPREAD", 1, 0, 1) ? "true" : "false") << ", " << mt
       << ">(psi, gblob, blob_bytes, geom, rank_base, ntiles,\n"
       << "    [&](double2* tile, const unsigned char* blob, uint64_t full_base) {\n"
       << "  (void)full_base;\n"
-      << body << "  });\n}\n";
+      << body << "  }, &tmap);\n}\n";
     return o.str();
 }
 
@@ -1052,6 +1058,76 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
     return QSV_OK;
 }
 
+// Tensor map of a pass's tile on `st` (QSV_TMA_TENSOR=0 disables): the tile bits form
+// runs of consecutive amplitude-index bits (the low run capped at 7 bits, others at 8, the
+// box limit of 256 elements); each of the first five runs, with the non-tile bits above it,
+// is one tensor dim whose box is the run; tile bits above the fifth run are iterated (at most
+// 2^3 copies per tile).  Encoded once per (step, state buffer) and cached in the program.
+void tile_tensor_map(const qsv_program* prog, const qsv_state* st, const Step& s, GeomArg& ga, TmaDesc& out) {
+    static const bool on = env_int("QSV_TMA_TENSOR", 1, 0, 1) != 0;
+    const Driver& d = driver();
+    if (!on || !d.encode_tiled)
+        return;
+    const int L = s.geom.L, l = st->n_local;
+    std::vector<int> bits;
+    for (int b = 0; b < L; ++b)
+        bits.push_back(b);
+    for (int i = 0; i < s.geom.nhigh; ++i)
+        bits.push_back(s.geom.high[i]);
+    std::vector<std::pair<int, int>> runs;  // (start bit, length)
+    for (int b : bits) {
+        const int limit = runs.size() == 1 ? 7 : 8;  // the low run's box counts doubles
+        if (!runs.empty() && runs.back().first + runs.back().second == b && runs.back().second < limit)
+            ++runs.back().second;
+        else
+            runs.push_back({b, 1});
+    }
+    if (runs.empty() || runs[0].first != 0)
+        return;
+    const int rank = std::min<int>(5, static_cast<int>(runs.size()));
+    std::vector<int> extra;
+    for (size_t r = rank; r < runs.size(); ++r)
+        for (int i = 0; i < runs[r].second; ++i)
+            extra.push_back(runs[r].first + i);
+    if (extra.size() > 3)
+        return;  // more than 8 copies per tile: the per-run bulk copies are as good
+    cuuint64_t gdim[5], gstride[4];
+    cuuint32_t box[5], estr[5] = {1, 1, 1, 1, 1};
+    uint32_t box_amps = 1;
+    for (int dd = 0; dd < rank; ++dd) {
+        const int lo = runs[dd].first;
+        const int hi = dd + 1 < rank ? runs[dd + 1].first : l;
+        if (hi - lo > 31)
+            return;  // a tensor dim holds at most 2^32 elements
+        gdim[dd] = (cuuint64_t{1} << (hi - lo)) * (dd == 0 ? 2 : 1);
+        box[dd] = (1u << runs[dd].second) * (dd == 0 ? 2 : 1);
+        box_amps <<= runs[dd].second;
+        if (dd > 0)
+            gstride[dd - 1] = (cuuint64_t{16} << lo);
+        ga.tm_s[dd] = lo;
+    }
+    const auto key = std::make_pair(static_cast<const void*>(&s), static_cast<const void*>(st->amps));
+    auto& cache = const_cast<qsv_program*>(prog)->tmaps;
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+        CUtensorMap tm;
+        if (d.encode_tiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, static_cast<cuuint32_t>(rank), st->amps, gdim,
+                           gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return;
+        static_assert(sizeof(CUtensorMap) == sizeof(TmaDesc), "tensor map size");
+        TmaDesc t;
+        std::memcpy(&t, &tm, sizeof(t));
+        it = cache.emplace(key, t).first;
+    }
+    out = it->second;
+    ga.tm_rank = rank;
+    ga.tm_nx = static_cast<int32_t>(extra.size());
+    for (size_t i = 0; i < extra.size(); ++i)
+        ga.tm_x[i] = extra[i];
+    ga.tm_box_amps = box_amps;
+}
+
 cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step, const unsigned char* d_blob,
                        uint64_t rank_base, cudaStream_t stream, const LaunchRange& rg) {
     const Step& s = prog->steps[step];
@@ -1099,7 +1175,11 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
     double2* psi = st->amps;
     uint32_t bb = s.blob_bytes;
     uint64_t rb = rank_base, nt = tiles;
-    void* args[] = {&psi, const_cast<unsigned char**>(&d_blob), &bb, &ga, &rb, &nt};
+    TmaDesc tmap{};
+    ga.tm_rank = 0;
+    if (!rg.fuse && ga.nreg == 0 && !ga.poison && jk.mt == 1)
+        tile_tensor_map(prog, st, s, ga, tmap);
+    void* args[] = {&psi, const_cast<unsigned char**>(&d_blob), &bb, &ga, &rb, &nt, &tmap};
     const CUresult r = d.launch(static_cast<CUfunction>(jk.func), static_cast<unsigned>(grid), 1, 1,
                                 static_cast<unsigned>(jk.nt), 1, 1, static_cast<unsigned>(smem),
                                 reinterpret_cast<CUstream>(stream), args, nullptr);

@@ -59,6 +59,23 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 
+// 5-D tensor-map tile copies (coordinates in elements; dim 0 counts doubles).
+__device__ __forceinline__ void tensor_load5(void* smem_dst, const TmaDesc* tmap, const int32_t (&c)[5],
+                                             uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tensor_store5(const TmaDesc* tmap, const int32_t (&c)[5], const void* smem_src) {
+    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(smem_src))
+                 : "memory");
+}
+
 __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
@@ -769,7 +786,7 @@ __device__ __forceinline__ uint64_t tile_base(uint64_t t, const GeomArg& g) {
 template <int K, int NT, int NBUF = kNumBuf, int PD = NBUF - 1, bool SPREAD = true, int MT = 1, typename Ops>
 __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const unsigned char* __restrict__ gblob,
                                               uint32_t blob_bytes, const GeomArg& geom, uint64_t rank_base,
-                                              uint64_t ntiles, Ops&& ops) {
+                                              uint64_t ntiles, Ops&& ops, const TmaDesc* tmap = nullptr) {
     // MT tile groups of NT threads per CTA (see QSV_LTID): group `sub` owns NBUF buffers
     // and mbarriers and processes tiles T * MT + sub of the CTA's tile sequence T.  All
     // groups run the same number of iterations (a group past the last tile still runs
@@ -807,7 +824,10 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         for (uint32_t i = threadIdx.x; i < blob_bytes / 16; i += NT * MT)
             dst[i] = __ldg(src + i);
     }
-    constexpr int NW = SPREAD ? NT / 32 : 1;  // warps of a group issuing TMA copies
+    // tensor-map mode: one thread issues a few box copies per tile instead of the warps
+    // issuing one bulk copy per contiguous run
+    const bool tens = tmap != nullptr && geom.tm_rank > 0;
+    const int NW = tens ? 1 : (SPREAD ? NT / 32 : 1);  // warps of a group issuing TMA copies
     if (threadIdx.x == 0) {
         for (int b = 0; b < MT * NBUF; ++b)
             mbar_init(&mbar_all[b], NW);
@@ -831,9 +851,37 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     auto tile_of = [&](uint64_t T) { return (T * MT + static_cast<uint64_t>(sub)) ^ txor; };
     // does this tile read (whole mode) or hold (mixed mode) data of the peer?
     auto remote_tile = [&](uint64_t base) { return fused && (geom.sv_tile || (base & svm) != sgm); };
+    // tensor copies: coordinates of the box that holds tile base `bb` (+ iterated bits e)
+    auto tm_coords = [&](uint64_t bb, int32_t (&c)[5]) {
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            if (d >= geom.tm_rank) {
+                c[d] = 0;
+                continue;
+            }
+            const int lo = geom.tm_s[d];
+            const uint64_t v = bb >> lo;
+            const int hi = d + 1 < geom.tm_rank ? geom.tm_s[d + 1] : 63;
+            c[d] = static_cast<int32_t>(v & ((1ull << (hi - lo)) - 1ull)) << (d == 0 ? 1 : 0);
+        }
+    };
     auto issue_load = [&](uint64_t t, int b) {
         const uint64_t base = tile_base(geom.tile0 + t, geom);
         double2* dst = bufs + b * TILE;
+        if (tens) {
+            if (lane == 0) {
+                mbar_expect_tx(&mbar[b], static_cast<uint32_t>(sizeof(double2) * TILE));
+                for (int e = 0; e < (1 << geom.tm_nx); ++e) {
+                    uint64_t bb = base;
+                    for (int i = 0; i < geom.tm_nx; ++i)
+                        bb |= static_cast<uint64_t>((e >> i) & 1) << geom.tm_x[i];
+                    int32_t c[5];
+                    tm_coords(bb, c);
+                    tensor_load5(dst + static_cast<uint32_t>(e) * geom.tm_box_amps, tmap, c, &mbar[b]);
+                }
+            }
+            return;
+        }
         if (lane == 0)
             mbar_expect_tx(&mbar[b], static_cast<uint32_t>(my_runs) * run_bytes);
         __syncwarp();
@@ -915,9 +963,21 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
                 }
                 __syncwarp();
             }
-            for (int k = lane; k < my_runs; k += 32) {
-                const int j = warp + NW * k;
-                bulk_store(psi + base + hi_off[j << m], tile + (j << RL), run_bytes);
+            if (tens) {
+                if (lane == 0)
+                    for (int e = 0; e < (1 << geom.tm_nx); ++e) {
+                        uint64_t bb = base;
+                        for (int i = 0; i < geom.tm_nx; ++i)
+                            bb |= static_cast<uint64_t>((e >> i) & 1) << geom.tm_x[i];
+                        int32_t c[5];
+                        tm_coords(bb, c);
+                        tensor_store5(tmap, c, tile + static_cast<uint32_t>(e) * geom.tm_box_amps);
+                    }
+            } else {
+                for (int k = lane; k < my_runs; k += 32) {
+                    const int j = warp + NW * k;
+                    bulk_store(psi + base + hi_off[j << m], tile + (j << RL), run_bytes);
+                }
             }
             bulk_commit();
         }
