@@ -59,21 +59,61 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 
-// 5-D tensor-map tile copies (coordinates in elements; dim 0 counts doubles).
-__device__ __forceinline__ void tensor_load5(void* smem_dst, const TmaDesc* tmap, const int32_t (&c)[5],
-                                             uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
-        "%6}], [%7];" ::"r"(smem_u32(smem_dst)),
-        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(bar))
-        : "memory");
+// Tensor-map tile copies of rank 1..5 (the instruction's dimensionality must match the
+// map's rank; coordinates in elements, dim 0 counts doubles).
+__device__ __forceinline__ void tensor_load(int rank, void* smem_dst, const TmaDesc* tmap, const int32_t (&c)[5],
+                                            uint64_t* bar) {
+    const uint32_t d = smem_u32(smem_dst), m = smem_u32(bar);
+    const uint64_t t = reinterpret_cast<uint64_t>(tmap);
+    switch (rank) {
+    case 1:
+        asm volatile("cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2}], [%3];"
+                     ::"r"(d), "l"(t), "r"(c[0]), "r"(m) : "memory");
+        break;
+    case 2:
+        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                     ::"r"(d), "l"(t), "r"(c[0]), "r"(c[1]), "r"(m) : "memory");
+        break;
+    case 3:
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+                     ::"r"(d), "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(m) : "memory");
+        break;
+    case 4:
+        asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                     ::"r"(d), "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(m) : "memory");
+        break;
+    default:
+        asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];"
+                     ::"r"(d), "l"(t), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(m) : "memory");
+        break;
+    }
 }
 
-__device__ __forceinline__ void tensor_store5(const TmaDesc* tmap, const int32_t (&c)[5], const void* smem_src) {
-    asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
-                     reinterpret_cast<uint64_t>(tmap)),
-                 "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(smem_u32(smem_src))
-                 : "memory");
+__device__ __forceinline__ void tensor_store(int rank, const TmaDesc* tmap, const int32_t (&c)[5], const void* smem_src) {
+    const uint32_t sp = smem_u32(smem_src);
+    const uint64_t t = reinterpret_cast<uint64_t>(tmap);
+    switch (rank) {
+    case 1:
+        asm volatile("cp.async.bulk.tensor.1d.global.shared::cta.tile.bulk_group [%0, {%1}], [%2];" ::"l"(t), "r"(c[0]),
+                     "r"(sp) : "memory");
+        break;
+    case 2:
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(t),
+                     "r"(c[0]), "r"(c[1]), "r"(sp) : "memory");
+        break;
+    case 3:
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(t),
+                     "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(sp) : "memory");
+        break;
+    case 4:
+        asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(t),
+                     "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(sp) : "memory");
+        break;
+    default:
+        asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(t),
+                     "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(sp) : "memory");
+        break;
+    }
 }
 
 __device__ __forceinline__ void bulk_wait_read_all() {
@@ -877,7 +917,7 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
                         bb |= static_cast<uint64_t>((e >> i) & 1) << geom.tm_x[i];
                     int32_t c[5];
                     tm_coords(bb, c);
-                    tensor_load5(dst + static_cast<uint32_t>(e) * geom.tm_box_amps, tmap, c, &mbar[b]);
+                    tensor_load(geom.tm_rank, dst + static_cast<uint32_t>(e) * geom.tm_box_amps, tmap, c, &mbar[b]);
                 }
             }
             return;
@@ -971,7 +1011,7 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
                             bb |= static_cast<uint64_t>((e >> i) & 1) << geom.tm_x[i];
                         int32_t c[5];
                         tm_coords(bb, c);
-                        tensor_store5(tmap, c, tile + static_cast<uint32_t>(e) * geom.tm_box_amps);
+                        tensor_store(geom.tm_rank, tmap, c, tile + static_cast<uint32_t>(e) * geom.tm_box_amps);
                     }
             } else {
                 for (int k = lane; k < my_runs; k += 32) {
