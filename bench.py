@@ -325,11 +325,14 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
         step(k)
     drain()
     barrier()
+    # the stream of circuits runs `e2e_steps` steps (default max(K, 8)): with three engines in
+    # flight, K = 3 would time mostly the pipeline's fill and drain, not its steady state
+    nsteps = args.e2e_steps or max(args.steps, 8)
     t0 = time.perf_counter()
-    for k in range(args.steps):
+    for k in range(nsteps):
         step(k)
     drain()
-    e2e_s = (time.perf_counter() - t0) / args.steps
+    e2e_s = (time.perf_counter() - t0) / nsteps
     if dist is not None:
         import torch
 
@@ -337,7 +340,7 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     # the result of the last step is on the host: check it is a normalised state
-    last = np.ctypeslib.as_array(C.cast(bufs[1 + (args.steps - 1) % ne], C.POINTER(C.c_double)), shape=(2 * N,))
+    last = np.ctypeslib.as_array(C.cast(bufs[1 + (nsteps - 1) % ne], C.POINTER(C.c_double)), shape=(2 * N,))
     local_norm = float(np.dot(last, last))
     for e in engines[1:]:
         e.close()
@@ -347,7 +350,7 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
            "stream events (H2D(k+1) | run(k) | D2H(k-1)); pinned host buffers, full state in and out"
            if ne > 1 else
            "qsim_engine_upload -> qsim_engine_run -> qsim_engine_download (pinned host buffers, full state in and out)")
-    return {"value": gates / e2e_s, "unit": "gates/s", "h2d_bytes_per_step": 16 * N * world,
+    return {"value": gates / e2e_s, "unit": "gates/s", "steps": nsteps, "h2d_bytes_per_step": 16 * N * world,
             "d2h_bytes_per_step": 16 * N * world, "seconds_per_step": e2e_s, "engines": ne,
             "host_norm_rank_shard": local_norm, "api": api}
 
@@ -444,6 +447,7 @@ def main():
     ap.add_argument("--no-extra-configs", action="store_true",
                     help="skip the other BASELINE.json configs (QFT-24, random-30 DAGC off, UCCSD-28, HEA-33)")
     ap.add_argument("--e2e-sequential", action="store_true", help="one engine, no copy/compute overlap")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="steps of the e2e stream (default max(K, 8))")
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per reference step")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds for the cpu_baseline sample")
     ap.add_argument("--cpu-min-gates", type=int, default=45, help="gates the cpu_baseline sample covers at least")
