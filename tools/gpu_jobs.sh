@@ -1,0 +1,37 @@
+#!/usr/bin/env bash
+# Reusable GPU jobs (run through gpurun; everything lands in gpurun_out/):
+#   tools/gpu_jobs.sh suite            1 GPU: pytest -m gpu, smoke, bench + reference arm, ncu launch
+#                                      list and a full capture of the heaviest pass (= tests/gpu_scripts/gpu_job.sh)
+#   tools/gpu_jobs.sh multi N          N GPUs: the multi-GPU suite, then bench lines at N GPUs for
+#                                      random-30 and (128 GiB per GPU) QFT-(32+log2 N) / random-(32+log2 N)
+#   tools/gpu_jobs.sh ab "SPECS" "ENV1" "ENV2" ...   kernel-switch A/B (tools/env_ab.sh)
+#   tools/gpu_jobs.sh fp64             measured DFMA / DMMA peaks (tools/fp64_peak.sh)
+#   tools/gpu_jobs.sh trace SPEC N     PipelineTrace of one N-GPU run (tools/trace_run.py)
+set -u
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+job=${1:-suite}; shift || true
+case "$job" in
+suite)
+  bash tests/gpu_scripts/gpu_job.sh ;;
+multi)
+  N=${1:-2}
+  timeout 2400 python -m pytest tests/test_gpu_multi.py -q -m gpu > gpurun_out/pytest_multi_n$N.log 2>&1
+  echo "multi pytest rc=$?"; tail -3 gpurun_out/pytest_multi_n$N.log
+  big=$((32 + $(python -c "import math;print(int(math.log2($N)))")))
+  for wl in random:30:20:2 qft:$big random:$big:20:2; do
+    extra=""; [ "$wl" != "random:30:20:2" ] && extra="--no-e2e --no-cpu-baseline"
+    timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+      --master-port 29521 bench.py --gpus $N --steps 2 --warmup 3 $extra --workload $wl \
+      > gpurun_out/n${N}_${wl//:/_}.json 2> gpurun_out/n${N}_${wl//:/_}.err
+    echo "$wl rc=$?"; tail -c 400 gpurun_out/n${N}_${wl//:/_}.json
+  done ;;
+ab)
+  ./tools/env_ab.sh "$@" 2>&1 | tee gpurun_out/ab.log ;;
+fp64)
+  ./tools/fp64_peak.sh ;;
+trace)
+  timeout 900 python tools/trace_run.py "$1" "${2:-2}" gpurun_out/trace.json ;;
+*)
+  echo "unknown job $job"; exit 2 ;;
+esac
