@@ -7,6 +7,7 @@
 #   tools/gpu_jobs.sh ab "SPECS" "ENV1" "ENV2" ...   kernel-switch A/B (tools/env_ab.sh)
 #   tools/gpu_jobs.sh fp64             measured DFMA / DMMA peaks (tools/fp64_peak.sh)
 #   tools/gpu_jobs.sh trace SPEC N     PipelineTrace of one N-GPU run (tools/trace_run.py)
+#   tools/gpu_jobs.sh swapncu N        ncu NVLink/DRAM bytes of rank 0's first P2P swap kernel (tools/ncu_rank0.sh)
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -32,6 +33,11 @@ fp64)
   ./tools/fp64_peak.sh ;;
 trace)
   timeout 900 python tools/trace_run.py "$1" "${2:-2}" gpurun_out/trace.json ;;
+swapncu)
+  N=${1:-2}
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29523 \
+    --no-python tools/ncu_rank0.sh --gpus $N --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/swapncu.log 2>&1
+  echo "swapncu rc=$?"; tail -5 gpurun_out/swapncu.log; cat gpurun_out/ncu_swap.csv | tail -8 ;;
 *)
   echo "unknown job $job"; exit 2 ;;
 esac
