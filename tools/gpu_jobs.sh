@@ -8,6 +8,7 @@
 #   tools/gpu_jobs.sh fp64             measured DFMA / DMMA peaks (tools/fp64_peak.sh)
 #   tools/gpu_jobs.sh trace SPEC N     PipelineTrace of one N-GPU run (tools/trace_run.py)
 #   tools/gpu_jobs.sh swapncu N        ncu NVLink/DRAM bytes of rank 0's first P2P swap kernel (tools/ncu_rank0.sh)
+#   tools/gpu_jobs.sh dmmancu          ncu --set full of a pass with DMMA16 ops (QSV_DMMA_MIN_PIPE=32, random-28)
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -38,6 +39,10 @@ swapncu)
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29523 \
     --no-python tools/ncu_rank0.sh --gpus $N --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/swapncu.log 2>&1
   echo "swapncu rc=$?"; tail -5 gpurun_out/swapncu.log; cat gpurun_out/ncu_swap.csv | tail -8 ;;
+dmmancu)
+  QSV_DMMA_MIN_PIPE=32 timeout 900 ncu --set full --import-source on --clock-control none -k regex:qsv_jit -c 1 \
+    -o gpurun_out/dmma_pass python tests/gpu_scripts/prof.py random:28:20:2 > gpurun_out/dmmancu.log 2>&1
+  echo "dmmancu rc=$?"; tail -3 gpurun_out/dmmancu.log ;;
 *)
   echo "unknown job $job"; exit 2 ;;
 esac
