@@ -868,12 +868,9 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
     // issuing one bulk copy per contiguous run
     const bool tens = tmap != nullptr && geom.tm_rank > 0;
     const int NW = tens ? 1 : (SPREAD ? NT / 32 : 1);  // warps of a group issuing TMA copies
-    // fused swap: the peer's runs arrive through per-lane cp.async (LDGSTS) copies whose
-    // completion each issuing lane signals with a counted (noinc) mbarrier arrival
-    const bool fused_ld = geom.peer != nullptr && !tens;
     if (threadIdx.x == 0) {
         for (int b = 0; b < MT * NBUF; ++b)
-            mbar_init(&mbar_all[b], fused_ld ? NW * 33 : NW);
+            mbar_init(&mbar_all[b], NW);
         fence_mbar_init();
     }
     __syncthreads();
@@ -923,35 +920,6 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
                     tensor_load(geom.tm_rank, dst + static_cast<uint32_t>(e) * geom.tm_box_amps, tmap, c, &mbar[b]);
                 }
             }
-            return;
-        }
-        if (fused_ld) {
-            // local runs by TMA (bytes counted by expect_tx), the peer's runs by all 32 lanes
-            // with 16-byte cp.async over NVLink (many loads in flight per warp)
-            uint32_t local_bytes = 0;
-            for (int k = 0; k < my_runs; ++k) {
-                const uint64_t idx = base + hi_off[(warp + NW * k) << m];
-                if ((idx & svm) == sgm)
-                    local_bytes += run_bytes;
-            }
-            if (lane == 0)
-                mbar_expect_tx(&mbar[b], local_bytes);
-            __syncwarp();
-            for (int k = 0; k < my_runs; ++k) {
-                const int j = warp + NW * k;
-                const uint64_t idx = base + hi_off[j << m];
-                double2* d = dst + (j << RL);
-                if ((idx & svm) == sgm) {
-                    if (lane == 0)
-                        bulk_load(d, psi + idx, run_bytes, &mbar[b]);
-                } else {
-                    const double2* src = geom.peer + (idx ^ svm);
-                    for (uint32_t e = lane; e < (1u << RL); e += 32)
-                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d + e)), "l"(src + e)
-                                     : "memory");
-                }
-            }
-            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&mbar[b])) : "memory");
             return;
         }
         if (lane == 0)
