@@ -931,13 +931,16 @@ JitPlan plan_kernels_mode(const std::vector<Step>& steps, const unsigned char* h
     return jp;
 }
 
-constexpr int kKernelsPerUnit = 6;
+// Kernels per NVRTC translation unit (QSV_JIT_UNIT overrides; every unit re-parses the
+// device source, so larger units amortise it, smaller ones spread over more host threads)
+int kernels_per_unit() { return env_int("QSV_JIT_UNIT", 6, 1, 256); }
 
 // NVRTC-compiles the kernels of `jp` in translation units of kKernelsPerUnit,
 // concurrently (no device needed).
 bool compile_kernels(const JitPlan& jp, std::vector<std::vector<char>>& cubins, std::string& err,
                      std::vector<std::string>* sources = nullptr) {
     const int nk = static_cast<int>(jp.bodies.size());
+    const int kKernelsPerUnit = kernels_per_unit();
     const int nunits = (nk + kKernelsPerUnit - 1) / kKernelsPerUnit;
     std::vector<std::string> srcs(nunits);
     for (int u = 0; u < nunits; ++u) {
@@ -1003,7 +1006,7 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
             *seconds = 0;
         return QSV_OK;
     }
-    const int per_unit = kKernelsPerUnit;
+    const int per_unit = kernels_per_unit();
     const int nunits = (nk + per_unit - 1) / per_unit;
     const std::vector<int>& kernel_k = jp.kernel_k;
     std::vector<std::vector<char>> cubins;
