@@ -9,7 +9,6 @@
 #   tools/gpu_jobs.sh trace SPEC N     PipelineTrace of one N-GPU run (tools/trace_run.py)
 #   tools/gpu_jobs.sh swapncu N        ncu NVLink/DRAM bytes of rank 0's first P2P swap kernel (tools/ncu_rank0.sh)
 #   tools/gpu_jobs.sh dmmancu          ncu --set full of a pass with DMMA16 ops (QSV_DMMA_MIN_PIPE=32, random-28)
-#   tools/gpu_jobs.sh nvlink [l]       NVLink bytes of one P2P swap from the driver's NVLink counters (2 GPUs)
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -44,8 +43,6 @@ dmmancu)
   QSV_DMMA_MIN_PIPE=32 timeout 900 ncu --set full --import-source on --clock-control none -k regex:qsv_jit -c 1 \
     -o gpurun_out/dmma_pass python tests/gpu_scripts/prof.py random:28:20:2 > gpurun_out/dmmancu.log 2>&1
   echo "dmmancu rc=$?"; tail -3 gpurun_out/dmmancu.log ;;
-nvlink)
-  timeout 600 python tools/nvlink_bytes.py ${1:-30} > gpurun_out/nvlink_bytes.json 2>&1; echo "nvlink rc=$?"; cat gpurun_out/nvlink_bytes.json ;;
 *)
   echo "unknown job $job"; exit 2 ;;
 esac
