@@ -551,7 +551,13 @@ def main():
     t_roof = sum(max(b / (hbm_peak * 1e9), f / (f64_peak * 1e12)) for b, f in zip(pass_bytes, pass_flops))
     nvl = sum(s["nvl_bytes"] for s in steps_info)
     t_roof += nvl / 770e9
-    norm = eng.norm_sq()
+    norm = eng.norm_sq()  # this rank's shard; summed over the ranks below (a whole-state check at every N)
+    if dist is not None:
+        import torch
+
+        tn = torch.tensor([norm], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tn, op=dist.ReduceOp.SUM)
+        norm = float(tn.item())
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -628,7 +634,7 @@ def main():
         "swap_ms_total": sum(swap_ms) if swap_ms else 0.0,
         # BBOP: (step time - local passes alone) / swaps alone, both from the per-step profile
         "swap_exposed_frac": ((ms_step - sum(pass_ms)) / sum(swap_ms)) if swap_ms and sum(swap_ms) > 0 else None,
-        "norm_error": abs(norm - 1.0) if world == 1 else None,
+        "norm_error": abs(norm - 1.0),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "configs": extra,
