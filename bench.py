@@ -253,7 +253,7 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
     strictly sequential copies)."""
     N = 1 << n_local
     L = pkg.load_qsim()
-    want = 1 if args.e2e_sequential else 3
+    want = 1 if args.e2e_sequential else max(1, args.e2e_engines)
     engines = [eng]
     while len(engines) < want:
         try:
@@ -448,6 +448,7 @@ def main():
                     help="skip the other BASELINE.json configs (QFT-24, random-30 DAGC off, UCCSD-28, HEA-33)")
     ap.add_argument("--e2e-sequential", action="store_true", help="one engine, no copy/compute overlap")
     ap.add_argument("--e2e-steps", type=int, default=0, help="steps of the e2e stream (default max(K, 8))")
+    ap.add_argument("--e2e-engines", type=int, default=3, help="engines (HBM states) the e2e stream rotates over")
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per reference step")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds for the cpu_baseline sample")
     ap.add_argument("--cpu-min-gates", type=int, default=45, help="gates the cpu_baseline sample covers at least")
