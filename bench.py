@@ -325,9 +325,9 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
         step(k)
     drain()
     barrier()
-    # the stream of circuits runs `e2e_steps` steps (default max(K, 8)): with three engines in
+    # the stream of circuits runs `e2e_steps` steps (default max(K, 16)): with three engines in
     # flight, K = 3 would time mostly the pipeline's fill and drain, not its steady state
-    nsteps = args.e2e_steps or max(args.steps, 8)
+    nsteps = args.e2e_steps or max(args.steps, 16)
     t0 = time.perf_counter()
     for k in range(nsteps):
         step(k)
@@ -447,7 +447,7 @@ def main():
     ap.add_argument("--no-extra-configs", action="store_true",
                     help="skip the other BASELINE.json configs (QFT-24, random-30 DAGC off, UCCSD-28, HEA-33)")
     ap.add_argument("--e2e-sequential", action="store_true", help="one engine, no copy/compute overlap")
-    ap.add_argument("--e2e-steps", type=int, default=0, help="steps of the e2e stream (default max(K, 8))")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="steps of the e2e stream (default max(K, 16))")
     ap.add_argument("--e2e-engines", type=int, default=3, help="engines (HBM states) the e2e stream rotates over")
     ap.add_argument("--ref-budget", type=float, default=12.0, help="seconds of CPU work per reference step")
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds for the cpu_baseline sample")
