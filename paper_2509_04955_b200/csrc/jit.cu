@@ -131,8 +131,12 @@ bool split_blocks() {
     const char* e = std::getenv("QSV_JIT_SPLIT");
     return e && e[0] == '1';
 }
+// Wide kernels (set while a kernel is generated): 11-qubit tiles whose register blocks hold
+// 8 amplitudes (rblock_k = 3) run 256 threads, one 8-member group each — twice the warps
+// per SM of the 16-member blocks at ~85 registers (QSV_JIT_WIDE=0 keeps 128 threads).
+thread_local bool t_wide = false;
 int threads_for_k(int K) {
-    if (K == 11 && split_blocks())
+    if (K == 11 && (split_blocks() || t_wide))
         return 256;
     return K >= 12 ? 256 : (K >= 8 ? 128 : (K >= 6 ? 64 : 32));
 }
@@ -848,9 +852,28 @@ namespace {
 // Distinct pass structures of a program -> kernel sources (host only).
 struct JitPlan {
     std::vector<std::string> bodies;
-    std::vector<int> kernel_k, kernel_minb, kernel_mt;
+    std::vector<int> kernel_k, kernel_minb, kernel_mt, kernel_wide;
     std::vector<int> jit_of_step;
 };
+
+// A pass qualifies for wide kernels when every register block holds <= 8 amplitudes and no
+// op needs a thread per 32-member group (dense k = 5).
+bool wide_pass(const Step& s, const unsigned char* blob) {
+    if (s.geom.K != 11 || split_blocks() || env_int("QSV_JIT_WIDE", 1, 0, 1) == 0)
+        return false;
+    const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
+    bool any_rb = false;
+    for (int i = 0; i < s.nops; ++i) {
+        if (ops[i].kind == QSV_OP_RBLOCK) {
+            if (ops[i].k > 3)
+                return false;
+            any_rb = true;
+        }
+        if ((ops[i].kind == QSV_OP_DENSE && ops[i].k == 5) || ops[i].kind == QSV_OP_DMMA16)
+            return false;
+    }
+    return any_rb;
+}
 
 // Dynamic SMEM of a specialised kernel: MT groups x NBUF tile buffers + the pass blob.
 size_t jit_tile_smem(int K, int mt) { return sizeof(double2) * static_cast<size_t>(mt) * tile_nbuf() * (size_t{1} << K); }
@@ -907,7 +930,12 @@ JitPlan plan_kernels_mode(const std::vector<Step>& steps, const unsigned char* h
         if (s.desc.kind != QSV_STEP_PASS || s.geom.K < 4)
             continue;
         int minb = 3;
-        int mt = jit_mt(s.geom.K);
+        const bool wide = wide_pass(s, host_blobs + s.blob_off);
+        t_wide = wide;
+        struct WideReset {
+            ~WideReset() { t_wide = false; }
+        } wide_reset;
+        int mt = wide ? 1 : jit_mt(s.geom.K);
         bool mt_ok = true;
         std::string body = gen_ops(s, host_blobs + s.blob_off, minb, mt, &mt_ok, class_mode);
         if (mt > 1 && (!mt_ok || jit_tile_smem(s.geom.K, mt) + s.blob_bytes > kSmemPerCta)) {
@@ -915,7 +943,7 @@ JitPlan plan_kernels_mode(const std::vector<Step>& steps, const unsigned char* h
             body = gen_ops(s, host_blobs + s.blob_off, minb, 1, nullptr, class_mode);
         }
         const std::string key = std::to_string(s.geom.K) + "|" + std::to_string(minb) + "|" + std::to_string(mt) +
-                                "|" + body;
+                                "|" + (wide ? "w|" : "|") + body;
         auto it = uniq.find(key);
         if (it == uniq.end()) {
             if (static_cast<int>(jp.bodies.size()) >= max_kernels)
@@ -925,6 +953,7 @@ JitPlan plan_kernels_mode(const std::vector<Step>& steps, const unsigned char* h
             jp.kernel_k.push_back(s.geom.K);
             jp.kernel_minb.push_back(minb);
             jp.kernel_mt.push_back(mt);
+            jp.kernel_wide.push_back(wide ? 1 : 0);
         }
         jp.jit_of_step[i] = it->second;
     }
@@ -945,9 +974,12 @@ bool compile_kernels(const JitPlan& jp, std::vector<std::vector<char>>& cubins, 
     std::vector<std::string> srcs(nunits);
     for (int u = 0; u < nunits; ++u) {
         std::string src = kDeviceSource;
-        for (int k = u * kKernelsPerUnit; k < std::min(nk, (u + 1) * kKernelsPerUnit); ++k)
+        for (int k = u * kKernelsPerUnit; k < std::min(nk, (u + 1) * kKernelsPerUnit); ++k) {
+            t_wide = jp.kernel_wide[k] != 0;
             src += kernel_source("qsv_jit_" + std::to_string(k), jp.kernel_k[k], jp.kernel_minb[k], jp.bodies[k],
                                  jp.kernel_mt[k]);
+            t_wide = false;
+        }
         srcs[u] = std::move(src);
     }
     cubins.assign(nunits, {});
@@ -1048,7 +1080,9 @@ int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
             d.set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                        static_cast<int>(std::min(tile_smem + kMaxBlobBytes, kSmemPerCta)));
             prog->jit_kernels[k].func = f;
+            t_wide = jp.kernel_wide[k] != 0;
             prog->jit_kernels[k].nt = threads_for_k(K) * mt;
+            t_wide = false;
             prog->jit_kernels[k].mt = mt;
             prog->jit_kernels[k].tile_smem = tile_smem;
         }
