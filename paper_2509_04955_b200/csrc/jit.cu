@@ -131,9 +131,10 @@ bool split_blocks() {
     const char* e = std::getenv("QSV_JIT_SPLIT");
     return e && e[0] == '1';
 }
-// Wide kernels (set while a kernel is generated): 11-qubit tiles whose register blocks hold
-// 8 amplitudes (rblock_k = 3) run 256 threads, one 8-member group each — twice the warps
-// per SM of the 16-member blocks at ~85 registers (QSV_JIT_WIDE=0 keeps 128 threads).
+// Wide kernels (set while a kernel is generated, QSV_JIT_WIDE=1): 11-qubit tiles whose
+// register blocks hold 8 amplitudes (rblock_k = 3) run 256 threads, one 8-member group each —
+// twice the warps per SM at 72-74 registers.  Measured equal to 128 threads (random-30 with
+// rblock_k = 3: 381.5 vs 380.5 ms, HEA-30 138.7 vs 136.5), so off by default.
 thread_local bool t_wide = false;
 int threads_for_k(int K) {
     if (K == 11 && (split_blocks() || t_wide))
@@ -859,7 +860,7 @@ struct JitPlan {
 // A pass qualifies for wide kernels when every register block holds <= 8 amplitudes and no
 // op needs a thread per 32-member group (dense k = 5).
 bool wide_pass(const Step& s, const unsigned char* blob) {
-    if (s.geom.K != 11 || split_blocks() || env_int("QSV_JIT_WIDE", 1, 0, 1) == 0)
+    if (s.geom.K != 11 || split_blocks() || env_int("QSV_JIT_WIDE", 0, 0, 1) == 0)
         return false;
     const TileOp* ops = reinterpret_cast<const TileOp*>(blob);
     bool any_rb = false;
