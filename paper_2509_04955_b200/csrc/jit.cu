@@ -347,7 +347,10 @@ std::string gen_ops(const Step& s, const unsigned char* blob, int& minb, int mt 
                 o << "  if ((full_base & " << opref << ".xctrl) == " << opref << ".xctrl) {\n";
             else if (op.xctrl)
                 o << "  if ((full_base & " << u64(op.xctrl) << ") == " << u64(op.xctrl) << ") {\n";
-            o << "  __syncthreads();\n";
+            // the first op needs no barrier: every thread waited on the tile's mbarrier, and
+            // the previous tile ended with one (QSV_JIT_FIRST_BARRIER=1 restores it for A/B)
+            if (i > 0 || env_int("QSV_JIT_FIRST_BARRIER", 0, 0, 1))
+                o << "  __syncthreads();\n";
         }
         switch (op.kind) {
         case QSV_OP_DENSE:
