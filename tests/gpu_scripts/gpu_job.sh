@@ -18,3 +18,5 @@ print(best[1])
 PY
 ) && echo "heaviest pass $IDX" && \
 ncu --set full --import-source on --clock-control none -k regex:"qsv_jit|pass_kernel" -s $IDX -c 1 -o gpurun_out/prof_full python tests/gpu_scripts/prof.py random:30:20:2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+python tests/gpu_scripts/prof.py hea:33:5:4 > gpurun_out/prof_hea33.log 2>&1; echo "prof hea33 rc=$?"; tail -2 gpurun_out/prof_hea33.log
+tail -2 gpurun_out/plain_h.log
