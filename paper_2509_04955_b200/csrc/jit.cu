@@ -1149,7 +1149,7 @@ void tile_tensor_map(const qsv_program* prog, const qsv_state* st, const Step& s
         ga.tm_s[dd] = lo;
     }
     const auto key = std::make_pair(static_cast<const void*>(&s), static_cast<const void*>(st->amps));
-    auto& cache = const_cast<qsv_program*>(prog)->tmaps;
+    auto& cache = prog->tmaps;
     auto it = cache.find(key);
     if (it == cache.end()) {
         CUtensorMap tm;

@@ -125,7 +125,7 @@ struct qsv_program {
     // one captured graph per state buffer it was run on
     std::map<const void*, cudaGraphExec_t> graphs;
     // tile tensor maps per (step, state buffer) (jit.cu tile_tensor_map)
-    std::map<std::pair<const void*, const void*>, qsv::TmaDesc> tmaps;
+    mutable std::map<std::pair<const void*, const void*>, qsv::TmaDesc> tmaps;
 };
 
 namespace qsv {
