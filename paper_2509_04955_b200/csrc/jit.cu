@@ -1219,7 +1219,7 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
     uint64_t rb = rank_base, nt = tiles;
     TmaDesc tmap{};
     ga.tm_rank = 0;
-    if (!rg.fuse && ga.nreg == 0 && !ga.poison && jk.mt == 1)
+    if (!rg.fuse && ga.nreg == 0 && jk.mt == 1)
         tile_tensor_map(prog, st, s, ga, tmap);
     void* args[] = {&psi, const_cast<unsigned char**>(&d_blob), &bb, &ga, &rb, &nt, &tmap};
     const CUresult r = d.launch(static_cast<CUfunction>(jk.func), static_cast<unsigned>(grid), 1, 1,

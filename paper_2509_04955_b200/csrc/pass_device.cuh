@@ -909,6 +909,13 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
         const uint64_t base = tile_base(geom.tile0 + t, geom);
         double2* dst = bufs + b * TILE;
         if (tens) {
+            if (geom.poison) {  // debug: NaN in the whole buffer before its tensor loads
+                const double nan = __longlong_as_double(0x7ff8dead00000000ll);
+                for (int e = lane; e < TILE; e += 32)
+                    dst[e] = make_double2(nan, nan);
+                fence_proxy_async();
+                __syncwarp();
+            }
             if (lane == 0) {
                 mbar_expect_tx(&mbar[b], static_cast<uint32_t>(sizeof(double2) * TILE));
                 for (int e = 0; e < (1 << geom.tm_nx); ++e) {

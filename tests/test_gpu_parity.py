@@ -313,5 +313,6 @@ def test_race_checks_poison_and_grid():
     tile order, pipeline phase and buffer reuse pattern)."""
     base = _sanitize_digests({})
     assert len(base) >= 6
-    for env in ({"QSV_DEBUG_POISON": "1"}, {"QSV_DEBUG_GRID": "1"}, {"QSV_DEBUG_GRID": "7", "QSV_DEBUG_POISON": "1"}):
+    for env in ({"QSV_DEBUG_POISON": "1"}, {"QSV_DEBUG_GRID": "1"}, {"QSV_DEBUG_GRID": "7", "QSV_DEBUG_POISON": "1"},
+                {"QSV_DEBUG_POISON": "1", "QSV_TMA_TENSOR": "0"}):  # tensor-map and per-run bulk copies
         assert _sanitize_digests(env) == base, env
