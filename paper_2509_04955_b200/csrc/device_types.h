@@ -117,6 +117,11 @@ struct GeomArg {
     uint64_t epoch;                 // flag value of iteration i: (epoch << 32) | (i + 1)
     int32_t sv, sv_tile, sv_tidx;   // sv_tidx (sv_tile = 0): tile-index bit of sv
     uint32_t sgbit;
+    // push mode (QSV_FUSE_SWAP=2): the swap is fused into the pass BEFORE it instead: loads are
+    // local (pre-swap layout) and the runs whose bit sv differs from sgbit are stored into the
+    // peer's shard at index ^ (1 << sv) (posted NVLink writes), after the twin flagged that it
+    // has loaded those slots
+    int32_t spush;
     // debug (QSV_DEBUG_POISON=1): every tile buffer run is filled with NaN before its
     // TMA load is issued, so an op that reads SMEM the load has not yet written (a broken
     // mbarrier / bulk-copy ordering) turns the result into NaN instead of a stale value

@@ -1200,6 +1200,7 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
         ga.sv_tile = rg.fuse->sv_tile;
         ga.sv_tidx = rg.fuse->sv_tidx;
         ga.sgbit = rg.fuse->sgbit;
+        ga.spush = rg.fuse->push;
     }
     const uint64_t all_tiles = st->size >> s.geom.K;
     const uint64_t region_tiles = apply_region(ga, rg, all_tiles);

@@ -946,7 +946,7 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
             const int j = warp + NW * k;
             const uint64_t idx = base + hi_off[j << m];
             const double2* src = psi + idx;
-            if (fused && (idx & svm) != sgm)
+            if (fused && !geom.spush && (idx & svm) != sgm)
                 src = geom.peer + (idx ^ svm);  // NVLink: the peer's slot of this amplitude run
             bulk_load(dst + (j << RL), src, run_bytes, &mbar[b]);
         }
@@ -1023,7 +1023,11 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
             } else {
                 for (int k = lane; k < my_runs; k += 32) {
                     const int j = warp + NW * k;
-                    bulk_store(psi + base + hi_off[j << m], tile + (j << RL), run_bytes);
+                    const uint64_t idx = base + hi_off[j << m];
+                    double2* dst = psi + idx;
+                    if (fused && geom.spush && (idx & svm) != sgm)
+                        dst = const_cast<double2*>(geom.peer) + (idx ^ svm);  // push: into the peer's slot
+                    bulk_store(dst, tile + (j << RL), run_bytes);
                 }
             }
             bulk_commit();

@@ -143,6 +143,7 @@ cudaError_t launch_variant(const qsv_state* st, const Step& step, const unsigned
         ga.sv_tile = rg.fuse->sv_tile;
         ga.sv_tidx = rg.fuse->sv_tidx;
         ga.sgbit = rg.fuse->sgbit;
+        ga.spush = rg.fuse->push;
     }
     const uint64_t region_tiles = apply_region(ga, rg, all_tiles);
     ga.tile0 = std::min(rg.tile0, region_tiles);

@@ -1582,6 +1582,29 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
             continue;
         }
         if (s.desc.kind == QSV_STEP_PASS) {
+            // BBOP push (QSV_FUSE_SWAP=2): a swap right after this pass rides in its stores —
+            // the runs that move are written into the peer's shard over NVLink
+            if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 0) == 2 && i + 1 < prog->steps.size() &&
+                prog->steps[i + 1].desc.kind == QSV_STEP_SWAP &&
+                (prog->jit_of_step.empty() || prog->jit_of_step[i] < 0 ||
+                 prog->jit_kernels[prog->jit_of_step[i]].mt == 1)) {
+                const qsv_step_desc& sw = prog->steps[i + 1].desc;
+                qsv::FusedSwap fs;
+                const int rc = qsv::fused_swap_prepare(st, sw.swap_global, sw.swap_local, s, &fs);
+                if (rc == QSV_OK) {
+                    fs.push = 1;
+                    qsv::LaunchRange rg;
+                    rg.fuse = &fs;
+                    QSV_CUDA(launch_step(st, prog, i, rank_base, rg, -2));
+                    ctx->trace_step = static_cast<int>(i + 1);
+                    if (int rc2 = qsv::fused_swap_finish(st, sw.swap_global); rc2 != QSV_OK)
+                        return rc2;
+                    ++i;
+                    continue;
+                }
+                if (rc != QSV_E_STATE)
+                    return rc;
+            }
             QSV_CUDA(launch_step(st, prog, i, rank_base));
             continue;
         }
@@ -1591,7 +1614,7 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
         // (QSV_FUSE_SWAP=1): bitwise equal to swap + pass, but its remote TMA loads reach
         // ~420 GB/s against the swap kernel's 695 (QFT-32 on 2 GPUs: 40.9 ms fused vs
         // 24.7 + 15.0 ms), and random-34 on 2 GPUs ran 4.5 s vs 2.8 s (profiles/r02_bbop.md)
-        if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 0) != 0 && i + 1 < prog->steps.size() &&
+        if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 0) == 1 && i + 1 < prog->steps.size() &&
             prog->steps[i + 1].desc.kind == QSV_STEP_PASS &&
             (prog->jit_of_step.empty() || prog->jit_of_step[i + 1] < 0 ||
              prog->jit_kernels[prog->jit_of_step[i + 1]].mt == 1)) {

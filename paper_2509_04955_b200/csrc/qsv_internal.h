@@ -138,6 +138,7 @@ struct FusedSwap {
     uint64_t epoch = 0;
     int sv = 0, sv_tile = 0, sv_tidx = 0;
     uint32_t sgbit = 0;
+    int push = 0;  // 1: fused into the pass before the swap (remote stores), else after (remote loads)
 };
 // Tile range and SM budget of one pass launch (default: every tile, every SM).
 struct LaunchRange {
@@ -181,6 +182,9 @@ void join_swap(qsv_ctx* ctx);
 // final) and fills `out`.  QSV_E_STATE when P2P is unavailable or the pass geometry does
 // not allow it (v in the pass's contiguous low run): run a plain swap instead.
 int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out);
+// Push mode: after the pass that pushed its half to the peer, order the compute stream after
+// a pair barrier (the peer's pushes into this shard have landed).
+int fused_swap_finish(qsv_state* st, int g);
 // k = 2 or 3 consecutive disjoint swaps (gs[i] <-> vs[i]) as one NVLink P2P all-to-all
 // among the 2^k ranks that differ in the g bits.  QSV_E_STATE when P2P is unavailable.
 int run_multi_swap(qsv_state* st, const int* gs, const int* vs, int k);

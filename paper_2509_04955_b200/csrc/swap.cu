@@ -361,6 +361,21 @@ int run_multi_swap(qsv_state* st, const int* gs, const int* vs, int k) {
     return e == cudaSuccess ? QSV_OK : fail_cuda("qsv_swap (multi): kernel", e);
 }
 
+int fused_swap_finish(qsv_state* st, int g) {
+    qsv_ctx* ctx = st->ctx;
+    const int peer = ctx->rank ^ (1 << (g - st->n_local));
+    cudaEventRecord(ctx->ev_a, ctx->stream);
+    cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_a, 0);
+    const int tb = trace_open(ctx, QSV_TRACE_BARRIER, -2, 1, ctx->comm_stream);
+    const ncclResult_t r = pair_barrier(ctx, peer);  // the peer's pushes into this shard are done
+    trace_close(ctx, tb, ctx->comm_stream);
+    if (r != ncclSuccess)
+        return fail_nccl("qsv_swap (push): barrier", r);
+    cudaEventRecord(ctx->ev_b, ctx->comm_stream);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
+    return QSV_OK;
+}
+
 int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out) {
     qsv_ctx* ctx = st->ctx;
     const int l = st->n_local;

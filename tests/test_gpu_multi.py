@@ -295,15 +295,16 @@ def test_shard_files_above_gather_cap(two, tmp_path):
     assert np.abs(np.concatenate(parts) - O.run_local(c)).max() <= 1e-10
 
 
+@pytest.mark.parametrize("mode", ["1", "2"])  # 1: into the pass after the swap (pull), 2: before (push)
 @pytest.mark.parametrize("spec", ["random:22:12:2", "qft:21", "hea:21:4:4", "uccsd:20:1500:3", "qaoa:20:2:1"])
-def test_fused_swap_bitwise_equals_plain_swap(two, spec, monkeypatch):
+def test_fused_swap_bitwise_equals_plain_swap(two, spec, mode, monkeypatch):
     """BBOP fused swap (the pass after a swap reads the peer's half over NVLink in its own
     tile loads, with per-CTA twin flags guarding the in-place overwrite) gives bitwise the
     result of the separate P2P swap + pass, and the oracle's to 1e-10."""
     c = pkg.Circuit.generate(spec)
     monkeypatch.setenv("QSV_FUSE_SWAP", "0")
     plain, rep0 = run_dist(c, 1, 14, 2)
-    monkeypatch.setenv("QSV_FUSE_SWAP", "1")
+    monkeypatch.setenv("QSV_FUSE_SWAP", mode)
     fused, rep1 = run_dist(c, 1, 14, 2)
     assert rep0.swaps == rep1.swaps >= 1
     assert np.array_equal(plain, fused)
@@ -317,9 +318,10 @@ def test_fused_swap_four_gpus(monkeypatch):
         c = pkg.Circuit.generate(spec)
         monkeypatch.setenv("QSV_FUSE_SWAP", "0")
         plain, _ = run_dist(c, 2, 14, 2)
-        monkeypatch.setenv("QSV_FUSE_SWAP", "1")
-        fused, _ = run_dist(c, 2, 14, 2)
-        assert np.array_equal(plain, fused)
+        for mode in ("1", "2"):
+            monkeypatch.setenv("QSV_FUSE_SWAP", mode)
+            fused, _ = run_dist(c, 2, 14, 2)
+            assert np.array_equal(plain, fused), mode
         assert np.abs(fused - O.run_local(c)).max() <= 1e-10
 
 
