@@ -1582,10 +1582,14 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
             continue;
         }
         if (s.desc.kind == QSV_STEP_PASS) {
-            // BBOP push (QSV_FUSE_SWAP=2): a swap right after this pass rides in its stores —
-            // the runs that move are written into the peer's shard over NVLink
-            if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 0) == 2 && i + 1 < prog->steps.size() &&
+            // BBOP push (QSV_FUSE_SWAP=2, default): a swap right after this pass rides in its
+            // stores — the runs that move are posted into the peer's shard over NVLink, so the
+            // pass's compute and HBM traffic hide under the transfer (QFT-32 on 2 GPUs: 25.8 ms
+            // for the fused step vs 11.9 + 24.9 ms; profiles/r02_bbop.md)
+            if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 2) == 2 && i + 1 < prog->steps.size() &&
                 prog->steps[i + 1].desc.kind == QSV_STEP_SWAP &&
+                // a run of swaps goes to the merged all-to-all instead
+                !(i + 2 < prog->steps.size() && prog->steps[i + 2].desc.kind == QSV_STEP_SWAP) &&
                 (prog->jit_of_step.empty() || prog->jit_of_step[i] < 0 ||
                  prog->jit_kernels[prog->jit_of_step[i]].mt == 1)) {
                 const qsv_step_desc& sw = prog->steps[i + 1].desc;
@@ -1609,11 +1613,12 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
             continue;
         }
         const int v = s.desc.swap_local, b = s.desc.chunk_log2;
-        // BBOP: the swap fused into the next pass (the pass streams the peer's half over
+        // BBOP pull: the swap fused into the next pass (the pass streams the peer's half over
         // NVLink in its own loads), when P2P is up and the pass geometry allows it.  Opt-in
         // (QSV_FUSE_SWAP=1): bitwise equal to swap + pass, but its remote TMA loads reach
         // ~420 GB/s against the swap kernel's 695 (QFT-32 on 2 GPUs: 40.9 ms fused vs
-        // 24.7 + 15.0 ms), and random-34 on 2 GPUs ran 4.5 s vs 2.8 s (profiles/r02_bbop.md)
+        // 24.7 + 15.0 ms), and random-34 on 2 GPUs ran 4.5 s vs 2.8 s (profiles/r02_bbop.md).
+        // The default is the push form above (QSV_FUSE_SWAP=2; 0 = separate swaps).
         if (evs == nullptr && !overlap && env_int("QSV_FUSE_SWAP", 0) == 1 && i + 1 < prog->steps.size() &&
             prog->steps[i + 1].desc.kind == QSV_STEP_PASS &&
             (prog->jit_of_step.empty() || prog->jit_of_step[i + 1] < 0 ||
