@@ -235,8 +235,10 @@ def test_pipeline_trace_nccl_chunks(two, monkeypatch):
 
 
 @pytest.mark.timeout(600)
-def test_pipeline_trace_p2p(two):
-    """The default NVLink P2P swap: one kernel per swap bracketed by the two pair barriers."""
+def test_pipeline_trace_p2p(two, monkeypatch):
+    """The NVLink P2P swap (not fused into a pass): one kernel per swap bracketed by the two
+    pair barriers."""
+    monkeypatch.setenv("QSV_FUSE_SWAP", "0")
     c = pkg.Circuit.generate("random:24:6:2")
     engines = _engines_in_threads(c, pkg.PlanOptions(), 2)
     try:
@@ -326,8 +328,9 @@ def test_fused_swap_four_gpus(monkeypatch):
 
 
 @pytest.mark.timeout(600)
-def test_fused_swap_in_trace(two, monkeypatch):
-    monkeypatch.setenv("QSV_FUSE_SWAP", "1")
+@pytest.mark.parametrize("mode", ["1", "2"])
+def test_fused_swap_in_trace(two, mode, monkeypatch):
+    monkeypatch.setenv("QSV_FUSE_SWAP", mode)
     c = pkg.Circuit.generate("qft:24")
     engines = _engines_in_threads(c, pkg.PlanOptions(), 2)
     try:
