@@ -1021,17 +1021,13 @@ __device__ __forceinline__ void pass_pipeline(double2* __restrict__ psi, const u
                         tensor_store(geom.tm_rank, tmap, c, tile + static_cast<uint32_t>(e) * geom.tm_box_amps);
                     }
             } else {
-                // push with bit sv inside the contiguous run: each run is stored in 2^(RL - sv)
-                // pieces of 2^sv amplitudes, alternately local and into the peer's shard
-                const int lp = (fused && geom.spush && geom.sv < RL) ? RL - geom.sv : 0;
-                for (int k = lane; k < (my_runs << lp); k += 32) {
-                    const int j = warp + NW * (k >> lp);
-                    const uint32_t off = static_cast<uint32_t>(k & ((1 << lp) - 1)) << (RL - lp);
-                    const uint64_t idx = base + hi_off[j << m] + off;
+                for (int k = lane; k < my_runs; k += 32) {
+                    const int j = warp + NW * k;
+                    const uint64_t idx = base + hi_off[j << m];
                     double2* dst = psi + idx;
                     if (fused && geom.spush && (idx & svm) != sgm)
                         dst = const_cast<double2*>(geom.peer) + (idx ^ svm);  // push: into the peer's slot
-                    bulk_store(dst, tile + (j << RL) + off, run_bytes >> lp);
+                    bulk_store(dst, tile + (j << RL), run_bytes);
                 }
             }
             bulk_commit();

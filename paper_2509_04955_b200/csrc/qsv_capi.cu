@@ -1594,7 +1594,7 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
                  prog->jit_kernels[prog->jit_of_step[i]].mt == 1)) {
                 const qsv_step_desc& sw = prog->steps[i + 1].desc;
                 qsv::FusedSwap fs;
-                const int rc = qsv::fused_swap_prepare(st, sw.swap_global, sw.swap_local, s, &fs, true);
+                const int rc = qsv::fused_swap_prepare(st, sw.swap_global, sw.swap_local, s, &fs);
                 if (rc == QSV_OK) {
                     fs.push = 1;
                     qsv::LaunchRange rg;

@@ -181,7 +181,7 @@ void join_swap(qsv_ctx* ctx);
 // first use), orders the compute stream after a pair barrier with the peer (both shards
 // final) and fills `out`.  QSV_E_STATE when P2P is unavailable or the pass geometry does
 // not allow it (v in the pass's contiguous low run): run a plain swap instead.
-int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out, bool push = false);
+int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out);
 // Push mode: after the pass that pushed its half to the peer, order the compute stream after
 // a pair barrier (the peer's pushes into this shard have landed).
 int fused_swap_finish(qsv_state* st, int g);

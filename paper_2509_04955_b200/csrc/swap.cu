@@ -376,19 +376,18 @@ int fused_swap_finish(qsv_state* st, int g) {
     return QSV_OK;
 }
 
-int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out, bool push) {
+int fused_swap_prepare(qsv_state* st, int g, int v, const Step& step, FusedSwap* out) {
     qsv_ctx* ctx = st->ctx;
     const int l = st->n_local;
     if (int rc = check_aborted(ctx, "qsv_swap (fused)"); rc != QSV_OK)
         return rc;
     if (!p2p_mode() || ctx->nranks < 2 || ctx->comm == nullptr || g < l || v < 0 || v >= l)
         return QSV_E_STATE;
-    // geometry: a pull needs v outside the pass's contiguous low run (a run has one source);
-    // a push splits its stores at bit v, so v >= 5 keeps the pieces >= 512 B
+    // geometry: v must not sit in the pass's contiguous low run (a run has one source)
     const PassGeom& pg = step.geom;
-    if (v < pg.L && (!push || v < 5))
+    if (v < pg.L)
         return QSV_E_STATE;
-    int sv_tile = v < pg.L ? 1 : 0, below = 0;
+    int sv_tile = 0, below = 0;
     for (int i = 0; i < pg.nhigh; ++i) {
         if (pg.high[i] == v)
             sv_tile = 1;
