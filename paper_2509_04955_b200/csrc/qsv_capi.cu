@@ -306,8 +306,12 @@ extern "C" int qsv_ctx_create(int device, int rank, int nranks, const void* comm
 namespace qsv {
 
 void abort_comm(qsv_ctx* ctx, const std::string& why) {
-    if (ctx->aborted.exchange(1) == 0)
-        ctx->abort_reason = why;
+    {
+        std::lock_guard<std::mutex> g(ctx->abort_lock);
+        if (ctx->abort_reason.empty())
+            ctx->abort_reason = why;  // the first reason wins
+    }
+    ctx->aborted.store(1);
     if (ctx->comm && ctx->comm_aborted.exchange(1) == 0)
         ncclCommAbort(ctx->comm);  // unblocks every NCCL kernel of this rank
 }
@@ -315,8 +319,12 @@ void abort_comm(qsv_ctx* ctx, const std::string& why) {
 int check_aborted(qsv_ctx* ctx, const char* what) {
     if (!ctx->aborted.load())
         return QSV_OK;
-    set_error(std::string(what) + " (rank " + std::to_string(ctx->rank) + "): collective aborted: " +
-              ctx->abort_reason);
+    std::string reason;
+    {
+        std::lock_guard<std::mutex> g(ctx->abort_lock);
+        reason = ctx->abort_reason;
+    }
+    set_error(std::string(what) + " (rank " + std::to_string(ctx->rank) + "): collective aborted: " + reason);
     return QSV_E_NCCL;
 }
 
@@ -347,7 +355,7 @@ int wait_stream(qsv_ctx* ctx, cudaStream_t stream, const char* what) {
             return QSV_E_CUDA;
         }
         if (ctx->aborted.load()) {
-            abort_comm(ctx, ctx->abort_reason);  // make sure the comm is torn down too
+            abort_comm(ctx, "aborted");  // make sure the comm is torn down too (the first reason is kept)
             // the NCCL kernels exit after the abort; let the stream drain
             cudaStreamSynchronize(stream);
             cudaGetLastError();

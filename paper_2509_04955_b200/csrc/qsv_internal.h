@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstdint>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -69,6 +70,7 @@ struct qsv_ctx {
     // wait; once set, every later call on this context fails with QSV_E_NCCL
     std::atomic<int> aborted{0};
     std::atomic<int> comm_aborted{0};
+    std::mutex abort_lock;      // guards abort_reason (written by the aborting thread)
     std::string abort_reason;
     // PipelineTrace: timing events around every pass launch, swap kernel,
     // send/recv chunk and copy-back while tracing is on (qsv_trace_enable)
