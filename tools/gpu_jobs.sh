@@ -9,6 +9,9 @@
 #   tools/gpu_jobs.sh trace SPEC N     PipelineTrace of one N-GPU run (tools/trace_run.py)
 #   tools/gpu_jobs.sh swapncu N        ncu NVLink/DRAM bytes of rank 0's first P2P swap kernel (tools/ncu_rank0.sh)
 #   tools/gpu_jobs.sh dmmancu          ncu --set full of a pass with DMMA16 ops (QSV_DMMA_MIN_PIPE=32, random-28)
+#   tools/gpu_jobs.sh fuseab N         N GPUs: the multi-GPU suite, then bench lines with separate
+#                                      (QSV_FUSE_SWAP=0) and push-fused (=2) swaps, and traces of
+#                                      QFT-32 / random-32 under 0, 1 (pull) and 2 (push) on 2 GPUs
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -43,6 +46,24 @@ dmmancu)
   QSV_DMMA_MIN_PIPE=32 timeout 900 ncu --set full --import-source on --clock-control none -k regex:qsv_jit -c 1 \
     -o gpurun_out/dmma_pass python tests/gpu_scripts/prof.py random:28:20:2 > gpurun_out/dmmancu.log 2>&1
   echo "dmmancu rc=$?"; tail -3 gpurun_out/dmmancu.log ;;
+fuseab)
+  N=${1:-2}
+  timeout 1800 python -m pytest tests/test_gpu_multi.py -q -m gpu > gpurun_out/pytest_multi_n$N.log 2>&1
+  echo "multi pytest rc=$?"; tail -3 gpurun_out/pytest_multi_n$N.log
+  big=$((33 + $(python -c "import math;print(int(math.log2($N)))")))
+  for wl in random:30:20:2 qft:$big random:$big:20:2; do
+    for m in 0 2; do
+      QSV_FUSE_SWAP=$m timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+        --master-port 29525 bench.py --gpus $N --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --workload $wl \
+        > gpurun_out/push_n${N}_${wl//:/_}_f$m.json 2>/dev/null
+      python -c "import json;d=json.loads(open('gpurun_out/push_n${N}_${wl//:/_}_f$m.json').read().strip().splitlines()[-1]);print('$wl fuse=$m', round(d['ms_per_step'],1), d.get('swap_exposed_frac'), d['config']['swaps'], d.get('norm_error'))"
+    done
+  done
+  if [ "$N" = 2 ]; then
+    for spec in qft:32 random:32:20:2; do for m in 0 1 2; do
+      QSV_FUSE_SWAP=$m timeout 600 python tools/trace_run.py $spec 2 gpurun_out/trace_${spec//:/_}_fuse$m.json 2>&1 | tail -1 | sed "s/^/[fuse=$m] /"
+    done; done
+  fi ;;
 *)
   echo "unknown job $job"; exit 2 ;;
 esac
