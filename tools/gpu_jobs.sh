@@ -7,7 +7,6 @@
 #   tools/gpu_jobs.sh ab "SPECS" "ENV1" "ENV2" ...   kernel-switch A/B (tools/env_ab.sh)
 #   tools/gpu_jobs.sh fp64             measured DFMA / DMMA peaks (tools/fp64_peak.sh)
 #   tools/gpu_jobs.sh trace SPEC N     PipelineTrace of one N-GPU run (tools/trace_run.py)
-#   tools/gpu_jobs.sh swapncu N        ncu NVLink/DRAM bytes of rank 0's first P2P swap kernel (tools/ncu_rank0.sh)
 #   tools/gpu_jobs.sh dmmancu          ncu --set full of a pass with DMMA16 ops (QSV_DMMA_MIN_PIPE=32, random-28)
 #   tools/gpu_jobs.sh fuseab N         N GPUs: the multi-GPU suite, then bench lines with separate
 #                                      (QSV_FUSE_SWAP=0) and push-fused (=2) swaps, and traces of
@@ -37,11 +36,6 @@ fp64)
   ./tools/fp64_peak.sh ;;
 trace)
   timeout 900 python tools/trace_run.py "$1" "${2:-2}" gpurun_out/trace.json ;;
-swapncu)
-  N=${1:-2}
-  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29523 \
-    --no-python tools/ncu_rank0.sh --gpus $N --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/swapncu.log 2>&1
-  echo "swapncu rc=$?"; tail -5 gpurun_out/swapncu.log; cat gpurun_out/ncu_swap.csv | tail -8 ;;
 dmmancu)
   QSV_DMMA_MIN_PIPE=32 timeout 900 ncu --set full --import-source on --clock-control none -k regex:qsv_jit -c 1 \
     -o gpurun_out/dmma_pass python tests/gpu_scripts/prof.py random:28:20:2 > gpurun_out/dmmancu.log 2>&1
