@@ -178,6 +178,7 @@ __global__ void digest_kernel(const unsigned long long* __restrict__ w, uint64_t
 }
 
 __global__ void set_one_kernel(double2* p) { *p = make_double2(1.0, 0.0); }
+__global__ void set_amp_kernel(double2* p, double re) { *p = make_double2(re, 0.0); }
 
 int reduce_grid(const qsv_ctx* ctx) { return ctx->sm_count * 8; }
 
@@ -596,11 +597,14 @@ extern "C" int qsv_state_set_basis(qsv_state* st, uint64_t global_index) {
         set_one_kernel<<<1, 1, 0, ctx->stream>>>(st->amps + (global_index & (st->size - 1)));
         QSV_CUDA(cudaGetLastError());
     }
+    st->is_basis = true;
+    st->basis = global_index;
     return QSV_OK;
 }
 
 extern "C" int qsv_state_upload(qsv_state* st, const double* host, uint64_t offset, uint64_t count) {
     QSV_REQUIRE(st != nullptr && (host != nullptr || count == 0), "qsv_state_upload: null argument");
+    st->is_basis = false;
     QSV_REQUIRE(offset <= st->size && count <= st->size - offset, "qsv_state_upload: range outside shard");
     QSV_CUDA(cudaSetDevice(st->ctx->device));
     QSV_CUDA(cudaMemcpyAsync(st->amps + offset, host, count * sizeof(double2), cudaMemcpyHostToDevice,
@@ -656,6 +660,7 @@ extern "C" int qsv_stream_wait_event(void* stream, void* ev) {
 extern "C" int qsv_state_device_ptr(qsv_state* st, void** ptr) {
     QSV_REQUIRE(st != nullptr && ptr != nullptr, "qsv_state_device_ptr: null argument");
     *ptr = st->amps;
+    st->is_basis = false;  // the caller may write through the pointer
     return QSV_OK;
 }
 
@@ -1510,8 +1515,66 @@ std::map<size_t, SwapOverlap> plan_overlap(const qsv_program* prog, int l) {
     return plans;
 }
 
+// Do all ranks hold the same basis state |x> (set_basis on every rank, nothing run since)?
+// Collective: one 16-byte max all-reduce of (v, -v), v = x or -1, so the ranks cannot diverge.
+int agree_basis(qsv_state* st, bool* same) {
+    qsv_ctx* ctx = st->ctx;
+    *same = false;
+    int64_t* d = reinterpret_cast<int64_t*>(ctx->d_coll + 128 * static_cast<size_t>(ctx->nranks) + 16);
+    const int64_t v = st->is_basis ? static_cast<int64_t>(st->basis) : -1;
+    int64_t h[2] = {v, -v};
+    // on the comm stream only: the agreement does not wait for the compute stream's queue
+    if (cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, ctx->comm_stream) != cudaSuccess) {
+        cudaGetLastError();
+        cudaMemsetAsync(d, 0xff, sizeof(h), ctx->comm_stream);  // (-1, -1): max = -1, never agreed
+    }
+    const ncclResult_t r = ncclAllReduce(d, d, 2, ncclInt64, ncclMax, ctx->comm, ctx->comm_stream);
+    if (r != ncclSuccess) {
+        qsv::abort_comm(ctx, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+        return qsv::check_aborted(ctx, "qsv_program_run: basis agreement");
+    }
+    if (int rc = qsv::wait_stream(ctx, ctx->comm_stream, "qsv_program_run: basis agreement"); rc != QSV_OK)
+        return rc;
+    QSV_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->comm_stream));
+    QSV_CUDA(cudaStreamSynchronize(ctx->comm_stream));
+    *same = h[0] >= 0 && h[0] == -h[1];
+    return QSV_OK;
+}
+
 int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
     qsv_ctx* ctx = st->ctx;
+    // Leading qubit swaps on a basis state |x>: every rank knows x, so the swaps become x with
+    // the swapped bits exchanged, set locally — no NVLink transfer.  The condition is rank-uniform
+    // (same program, same env); the state test is agreed collectively.
+    size_t first = 0;
+    bool basis_start = false;
+    if (evs == nullptr && ctx->nranks > 1 && ctx->comm != nullptr && !prog->steps.empty() &&
+        prog->steps[0].desc.kind == QSV_STEP_SWAP && env_int("QSV_BASIS_SWAPS", 1) != 0) {
+        QSV_CUDA(cudaSetDevice(ctx->device));
+        if (int rc = agree_basis(st, &basis_start); rc != QSV_OK)
+            return rc;
+    }
+    st->is_basis = false;  // the program below modifies the shard
+    if (basis_start) {
+        uint64_t x = st->basis;
+        while (first < prog->steps.size() && prog->steps[first].desc.kind == QSV_STEP_SWAP) {
+            const int g = prog->steps[first].desc.swap_global, v = prog->steps[first].desc.swap_local;
+            const uint64_t bg = (x >> g) & 1ull, bv = (x >> v) & 1ull;
+            if (bg != bv)
+                x ^= (1ull << g) | (1ull << v);
+            ++first;
+        }
+        if (first > 0 && x != st->basis) {
+            // move the single 1 from |basis> to |x> (the rest of every shard is already zero)
+            const uint64_t lmask = st->size - 1, me = static_cast<uint64_t>(ctx->rank);
+            QSV_CUDA(cudaSetDevice(ctx->device));
+            if ((st->basis >> st->n_local) == me)
+                set_amp_kernel<<<1, 1, 0, ctx->stream>>>(st->amps + (st->basis & lmask), 0.0);
+            if ((x >> st->n_local) == me)
+                set_amp_kernel<<<1, 1, 0, ctx->stream>>>(st->amps + (x & lmask), 1.0);
+            QSV_CUDA(cudaGetLastError());
+        }
+    }
     const uint64_t rank_base = static_cast<uint64_t>(ctx->rank) << st->n_local;
     const bool overlap = evs == nullptr && env_int("QSV_OVERLAP", 0) != 0;
     const int reserve = std::max(0, env_int("QSV_OVERLAP_RESERVE_SMS", 8));
@@ -1543,7 +1606,7 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
     for (const auto& kv : p2p_plan)
         if (kv.second.pre_begin < kv.first)
             pre_start[kv.second.pre_begin] = kv.first;
-    for (size_t i = 0; i < prog->steps.size(); ++i) {
+    for (size_t i = first; i < prog->steps.size(); ++i) {
         const qsv::Step& s = prog->steps[i];
         ctx->trace_step = static_cast<int>(i);
         if (evs)
@@ -1774,6 +1837,7 @@ extern "C" int qsv_program_run(qsv_state* st, qsv_program* prog) {
         prog->graphs[st->amps] = ge;
         return QSV_OK;
     }
+    st->is_basis = false;
     QSV_CUDA(cudaGraphLaunch(it->second, ctx->stream));
     return QSV_OK;
 }
@@ -1811,6 +1875,7 @@ extern "C" int qsv_program_step_cost(qsv_program* prog, int i, double* hbm_bytes
 extern "C" int qsv_apply_fused(qsv_state* st, int k, const int* targets, uint64_t ctrl_mask,
                                const double* mat) {
     QSV_REQUIRE(st != nullptr && targets != nullptr && mat != nullptr, "qsv_apply_fused: null argument");
+    st->is_basis = false;
     QSV_REQUIRE(k >= 1 && k <= QSV_MAX_DENSE_K, "qsv_apply_fused: k must be in [1, 5] (SPEC:89)");
     qsv_ctx* ctx = st->ctx;
     const int n_local = st->n_local;
@@ -1960,5 +2025,6 @@ extern "C" int qsv_state_digest(qsv_state* st, uint64_t* out) {
 
 extern "C" int qsv_swap(qsv_state* st, int g, int v, int chunk_log2, int nbuf) {
     QSV_REQUIRE(st != nullptr, "qsv_swap: null state");
+    st->is_basis = false;
     return qsv::run_swap(st, g, v, chunk_log2, nbuf);
 }

@@ -102,6 +102,11 @@ struct qsv_state {
     std::vector<double2*> peer_amps;   // per rank, nullptr = not mapped
     std::vector<char> peer_ipc;        // 1 = opened with cudaIpcOpenMemHandle (close on free)
     uint64_t fused_epoch = 0;          // fused swaps run on this buffer (flag epochs)
+    // the shard holds the basis state |basis> set by qsv_state_set_basis and nothing has
+    // touched it since: leading qubit swaps of a program then relabel the index instead of
+    // moving data (a swap maps a basis state to a basis state)
+    bool is_basis = false;
+    uint64_t basis = 0;
 };
 
 namespace qsv {

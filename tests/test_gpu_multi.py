@@ -362,3 +362,41 @@ def test_merged_swaps_four_gpus(spec, monkeypatch):
     merged, _ = run_dist(c, 2, 14, 2)
     assert np.array_equal(pairwise, merged)
     assert np.abs(merged - O.run_local(c)).max() <= 1e-10
+
+
+def _qft_from_basis_on_engines(n, x, runs, patch_rank=None):
+    """set_basis(x) on both ranks, then `runs` QFT runs; patch_rank uploads an empty patch on
+    that rank only (its shard is no longer known to be a basis state, the other's is)."""
+    c = pkg.Circuit.generate(f"qft:{n}")
+    engines = _engines_in_threads(c, pkg.PlanOptions(), 2)
+    try:
+        def go(e):
+            e.set_basis(x)
+            if patch_rank is not None and e is engines[patch_rank]:
+                e.upload(np.zeros(0, dtype=np.complex128))
+            for _ in range(runs):
+                e.run()
+            e.sync()
+        _run_all(engines, go)
+        return np.concatenate([e.download() for e in engines])
+    finally:
+        for e in engines:
+            e.close()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("x", [0x2A5A5A, 0x15A5A5, 0])
+def test_leading_swaps_on_basis_state(two, x, monkeypatch):
+    """A program that starts with qubit swaps, run on a basis state |x> (set_basis on every
+    rank): the swaps become a relabelled basis index — no NVLink transfer — and the result is
+    bitwise the transferred one.  A second run (no longer a basis state) and a rank whose
+    shard was written since set_basis (the ranks must agree) both move data as usual."""
+    n = 22
+    monkeypatch.setenv("QSV_BASIS_SWAPS", "0")
+    plain = _qft_from_basis_on_engines(n, x, 1)
+    twice_plain = _qft_from_basis_on_engines(n, x, 2)
+    monkeypatch.setenv("QSV_BASIS_SWAPS", "1")
+    assert np.array_equal(_qft_from_basis_on_engines(n, x, 1), plain)
+    assert np.array_equal(_qft_from_basis_on_engines(n, x, 2), twice_plain)
+    assert np.array_equal(_qft_from_basis_on_engines(n, x, 1, patch_rank=1), plain)
+    assert np.abs(plain - qft_basis_expected(n, x, 0, 1 << n)).max() <= 1e-10

@@ -11,6 +11,8 @@
 #   tools/gpu_jobs.sh fuseab N         N GPUs: the multi-GPU suite, then bench lines with separate
 #                                      (QSV_FUSE_SWAP=0) and push-fused (=2) swaps, and traces of
 #                                      QFT-32 / random-32 under 0, 1 (pull) and 2 (push) on 2 GPUs
+#   tools/gpu_jobs.sh basisab N        N GPUs: the multi-GPU suite, then QFT bench lines with leading
+#                                      swaps on the basis start moved (QSV_BASIS_SWAPS=0) or relabelled (=1)
 set -u
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
@@ -58,6 +60,19 @@ fuseab)
       QSV_FUSE_SWAP=$m timeout 600 python tools/trace_run.py $spec 2 gpurun_out/trace_${spec//:/_}_fuse$m.json 2>&1 | tail -1 | sed "s/^/[fuse=$m] /"
     done; done
   fi ;;
+basisab)
+  N=${1:-2}
+  timeout 1800 python -m pytest tests/test_gpu_multi.py -q -m gpu > gpurun_out/pytest_multi_n$N.log 2>&1
+  echo "multi pytest rc=$?"; tail -3 gpurun_out/pytest_multi_n$N.log
+  big=$((33 + $(python -c "import math;print(int(math.log2($N)))")))
+  for wl in qft:$big qft:30; do
+    for b in 0 1; do
+      QSV_BASIS_SWAPS=$b timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+        --master-port 29527 bench.py --gpus $N --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-extra-configs --workload $wl \
+        > gpurun_out/basis_n${N}_${wl//:/_}_b$b.json 2>/dev/null
+      python -c "import json;d=json.loads(open('gpurun_out/basis_n${N}_${wl//:/_}_b$b.json').read().strip().splitlines()[-1]);print('$wl basis_swaps=$b', round(d['ms_per_step'],1), d.get('swap_exposed_frac'), d['config']['swaps'], d.get('norm_error'))"
+    done
+  done ;;
 *)
   echo "unknown job $job"; exit 2 ;;
 esac
