@@ -123,7 +123,10 @@ const char* qsv_last_error(void);
 int qsv_state_alloc(qsv_ctx* ctx, int n_local, qsv_state** out, size_t* bytes);
 int qsv_state_free(qsv_state* st);
 /* Sets the distributed state to the basis state |global_index> (SPEC:392:
- * "|0...0> constructed"); ranks not owning the index get all zeros. */
+ * "|0...0> constructed"); ranks not owning the index get all zeros.  Every rank passes the same
+ * index.  The state remembers it until the next run, upload, apply, swap or device_ptr call: a
+ * multi-rank program that then starts with qubit swaps relabels the index instead of moving the
+ * shard (the ranks agree on it with one 16-byte all-reduce; QSV_BASIS_SWAPS=0 disables it). */
 int qsv_state_set_basis(qsv_state* st, uint64_t global_index);
 /* Host <-> device copies of `count` amplitudes starting at local `offset`,
  * interleaved (re, im) doubles.  Stream-ordered; host memory should be pinned
@@ -140,7 +143,8 @@ int qsv_event_create(void** ev);
 int qsv_event_destroy(void* ev);
 int qsv_event_record(void* ev, void* stream);
 int qsv_stream_wait_event(void* stream, void* ev);
-/* Raw device pointer of the shard (double2*), for interop/tests. */
+/* Raw device pointer of the shard (double2*), for interop/tests.  Fetch it after
+ * qsv_state_set_basis if you write through it (the call forgets the basis-state mark). */
 int qsv_state_device_ptr(qsv_state* st, void** ptr);
 /* Pinned host buffers for the upload/download paths. */
 int qsv_host_alloc(size_t bytes, void** ptr);
