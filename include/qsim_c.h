@@ -45,7 +45,8 @@ typedef struct qsim_plan_opts {
     int32_t register_blocks;  /* group native gates on <= 4 qubits (RBLOCK)     */
     double pass_budget;       /* DP cost units per amplitude per pass           */
     int32_t rblock_k;         /* register-block width: 3 or 4 qubits            */
-    int32_t jit;              /* NVRTC-specialised pass kernels (1) or the interpreter (0) */
+    int32_t jit;              /* NVRTC-specialised pass kernels (1), compiled in the background with
+                                 interpreted runs until they load (2), or the interpreter (0) */
     int32_t relabel;          /* tile-qubit relabel at pass ends: 0 off, 1 auto, 2 always */
     double max_sweeps;        /* SMEM sweeps of the tile per pass                */
     int32_t list_schedule;    /* single rank: also try a DAG list schedule       */
@@ -126,6 +127,8 @@ int qsim_engine_step_info(qsim_engine* e, int i, int* kind, int* nops, double* h
 int qsim_engine_profile(qsim_engine* e, float* ms_per_step);
 /* JIT statistics: distinct specialised kernels and compile seconds (0 = cache hits). */
 int qsim_engine_jit_info(qsim_engine* e, int* kernels, double* seconds);
+/* Waits for the engine's background compile (jit = 2) and adopts its kernels. */
+int qsim_engine_jit_wait(qsim_engine* e);
 
 /* ---- SPEC-level passes (reference semantics) ---- */
 typedef struct qsim_fusion_stats {

@@ -246,6 +246,16 @@ int qsv_program_free(qsv_program* prog);
  * *seconds receives the compile time (0 for disk-cache hits).  Returns
  * QSV_E_STATE when NVRTC is unavailable (the program stays valid). */
 int qsv_program_jit(qsv_program* prog, int max_kernels, double* seconds);
+/* The same specialisation on a background host thread: runs of the program use the interpreter
+ * kernel until the compile has finished, and the first run after that switches to the
+ * specialised kernels (results agree to rounding, not bitwise, across the switch).  Single-rank
+ * contexts only; on a multi-rank context this compiles synchronously, so that every rank
+ * switches at the same run. */
+int qsv_program_jit_async(qsv_program* prog, int max_kernels);
+/* Adopts a finished background compile (block != 0: waits for it).  *done = 1 once no compile
+ * is pending; *seconds = compile + load time of the adopted kernels.  Returns the compile's error
+ * if it failed (the program keeps the interpreter). */
+int qsv_program_jit_wait(qsv_program* prog, int block, int* done, double* seconds);
 int qsv_program_jit_info(qsv_program* prog, int* kernels, int* steps_jitted);
 /* Host-only dry run of qsv_program_create's validation and tile compilation
  * (no device needed): returns QSV_OK iff the program would be accepted for

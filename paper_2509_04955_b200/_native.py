@@ -160,7 +160,7 @@ class PlanOptions:
     pass_budget: float = 120.0
     register_blocks: bool = True
     rblock_k: int = 4
-    jit: bool = True
+    jit: int = True  # True/1 specialised kernels, 2 compiled in the background (interpreted runs until loaded), 0 off
     relabel: int = 1  # 0 off, 1 auto (kept when it saves passes), 2 always
     max_sweeps: float = 8.0
     list_schedule: bool = True
@@ -172,7 +172,7 @@ class PlanOptions:
         o = qsim_plan_opts()
         load_qsim().qsim_default_opts(C.byref(o))
         return cls(o.tile_k, o.min_low, o.fuse_k, bool(o.fusion), bool(o.multi_op_passes),
-                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k, bool(o.jit),
+                   o.chunk_log2, o.nbuf, o.pass_budget, bool(o.register_blocks), o.rblock_k, o.jit if o.jit == 2 else bool(o.jit),
                    int(o.relabel), o.max_sweeps, bool(o.list_schedule), o.jit_max_kernels,
                    int(o.logical_swaps))
 
@@ -418,6 +418,10 @@ class Engine:
         k, s = C.c_int(), C.c_double()
         _check(load_qsim().qsim_engine_jit_info(self._h, C.byref(k), C.byref(s)), "jit_info")
         return {"kernels": k.value, "seconds": s.value}
+
+    def jit_wait(self):
+        """Waits for a background compile (PlanOptions(jit=2)) and switches to its kernels."""
+        _check(load_qsim().qsim_engine_jit_wait(self._h), "jit_wait")
 
     def profile(self) -> list[float]:
         n = load_qsim().qsim_engine_nsteps(self._h)

@@ -70,8 +70,11 @@ class Engine {
     Engine& operator=(const Engine&) = delete;
 
     const Plan& plan() const { return plan_; }
-    double jit_seconds() const { return jit_seconds_; }
-    int jit_kernels() const { return jit_kernels_; }
+    // live figures: a background compile (PlanOptions::jit_async) counts once it is adopted
+    double jit_seconds() const;
+    int jit_kernels() const;
+    // waits for a background compile and adopts it (no-op otherwise)
+    void jit_wait() const;
     qsv_program* program() const { return prog_; }
     // Enqueues the whole circuit on the context stream (asynchronous).
     void run(DeviceState& st) const;
@@ -80,8 +83,6 @@ class Engine {
     DeviceContext& ctx_;
     Plan plan_;
     qsv_program* prog_ = nullptr;
-    double jit_seconds_ = 0.0;
-    int jit_kernels_ = 0;
 };
 
 } // namespace qsim

@@ -71,6 +71,7 @@ struct PlanOptions {
     int chunk_log2 = 26;      // BBOP batch: 2^b amplitudes per swap message; 1 GiB NCCL messages reach ~530 GB/s on NVLink 5 vs ~275 GB/s at 2^22
     int nbuf = 2;             // BBOP buffers B (default 2)
     bool jit = true;          // NVRTC-specialised pass kernels (falls back to the interpreter kernel)
+    bool jit_async = false;   // compile them on a background thread; runs interpret until they load
     int jit_max_kernels = 8192; // distinct pass structures compiled at most (the rest interpreted)
     int logical_swaps = 0;    // SWAP gates (CX triples) as free relabellings: 0 off, 1 when the
                               // time model prefers it, 2 always (tests)

@@ -65,6 +65,7 @@ qsim::PlanOptions to_opts(const qsim_plan_opts* o) {
     p.pass_budget = o->pass_budget;
     p.rblock_k = o->rblock_k;
     p.jit = o->jit != 0;
+    p.jit_async = o->jit == 2;
     p.relabel = o->relabel;
     p.max_sweeps = o->max_sweeps;
     p.list_schedule = o->list_schedule != 0;
@@ -122,7 +123,7 @@ void qsim_default_opts(qsim_plan_opts* out) {
     out->nbuf = p.nbuf;
     out->pass_budget = p.pass_budget;
     out->rblock_k = p.rblock_k;
-    out->jit = p.jit;
+    out->jit = p.jit ? (p.jit_async ? 2 : 1) : 0;
     out->relabel = p.relabel;
     out->max_sweeps = p.max_sweeps;
     out->list_schedule = p.list_schedule;
@@ -652,6 +653,14 @@ void qsim_memtrack_script(const long long* ops, int nops, int nranks, unsigned l
         for (int p = 0; p < 2; ++p)
             peaks[2 * r + p] = peak_bytes(r, static_cast<Phase>(p));
     unregister_thread();
+}
+
+int qsim_engine_jit_wait(qsim_engine* e) {
+    return guard([&] {
+        REQUIRE(e, "qsim_engine_jit_wait: null engine");
+        e->eng->jit_wait();
+        return QSV_OK;
+    });
 }
 
 int qsim_engine_jit_info(qsim_engine* e, int* kernels, double* seconds) {

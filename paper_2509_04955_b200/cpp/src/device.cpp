@@ -91,11 +91,10 @@ Engine::Engine(DeviceContext& ctx, const Circuit& c, const PlanOptions& opt) : c
                                  plan_.pool.size() / 2, &prog_),
               "qsv_program_create");
     if (o.jit && o.jit_max_kernels > 0) {
-        const int rc = qsv_program_jit(prog_, o.jit_max_kernels, &jit_seconds_);
-        if (rc == QSV_OK) {
-            int steps = 0;
-            qsv_program_jit_info(prog_, &jit_kernels_, &steps);
-        } else {
+        double secs = 0;
+        const int rc = o.jit_async ? qsv_program_jit_async(prog_, o.jit_max_kernels)
+                                   : qsv_program_jit(prog_, o.jit_max_kernels, &secs);
+        if (rc != QSV_OK) {
             static bool warned = false;
             if (!warned) {
                 std::fprintf(stderr, "qsim: JIT unavailable, using the interpreter pass kernel (%s)\n",
@@ -107,6 +106,25 @@ Engine::Engine(DeviceContext& ctx, const Circuit& c, const PlanOptions& opt) : c
 }
 
 Engine::~Engine() { qsv_program_free(prog_); }
+
+double Engine::jit_seconds() const {
+    int done = 0;
+    double s = 0;
+    qsv_program_jit_wait(prog_, 0, &done, &s);
+    return s;
+}
+
+int Engine::jit_kernels() const {
+    int done = 0, k = 0, steps = 0;
+    qsv_program_jit_wait(prog_, 0, &done, nullptr);
+    qsv_program_jit_info(prog_, &k, &steps);
+    return k;
+}
+
+void Engine::jit_wait() const {
+    int done = 0;
+    qsv_check(qsv_program_jit_wait(prog_, 1, &done, nullptr), "qsv_program_jit_wait");
+}
 
 void Engine::run(DeviceState& st) const { qsv_check(qsv_program_run(st.get(), prog_), "qsv_program_run"); }
 

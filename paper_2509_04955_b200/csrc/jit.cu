@@ -1028,76 +1028,155 @@ int jit_check(const std::vector<Step>& steps, const unsigned char* host_blobs, i
     return QSV_OK;
 }
 
-int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
+struct JitBuild {
+    std::vector<int> jit_of_step;
+    std::vector<JitKernel> kernels;
+    std::vector<void*> modules;  // CUmodule
+    double seconds = 0;
+    int rc = QSV_OK;
+    std::string err;
+};
+
+namespace {
+
+// Plans, compiles and loads the program's specialised kernels into `b`.  Reads only the
+// program's immutable steps / blobs / device, so it can run on a background thread.
+void jit_build(const qsv_program* prog, int max_kernels, JitBuild& b) {
     const auto t0 = std::chrono::steady_clock::now();
+    auto fail = [&](int rc, const std::string& why) {
+        const Driver& d = driver();
+        for (void* m : b.modules)
+            d.unload(static_cast<CUmodule>(m));
+        b.modules.clear();
+        b.kernels.clear();
+        b.jit_of_step.assign(prog->steps.size(), -1);
+        b.rc = rc;
+        b.err = why;
+    };
     std::string why;
-    if (!jit_available(why)) {
-        set_error("qsv_program_jit: " + why);
-        return QSV_E_STATE;
-    }
+    if (!jit_available(why))
+        return fail(QSV_E_STATE, "qsv_program_jit: " + why);
     JitPlan jp = plan_kernels(prog->steps, prog->host_blobs.data(), max_kernels);
-    prog->jit_of_step = jp.jit_of_step;
+    b.jit_of_step = jp.jit_of_step;
     const int nk = static_cast<int>(jp.bodies.size());
-    if (nk == 0) {
-        if (seconds)
-            *seconds = 0;
-        return QSV_OK;
-    }
+    if (nk == 0)
+        return;
     const int per_unit = kernels_per_unit();
     const int nunits = (nk + per_unit - 1) / per_unit;
     const std::vector<int>& kernel_k = jp.kernel_k;
     std::vector<std::vector<char>> cubins;
     std::vector<std::string> srcs;
     std::string err;
-    if (!compile_kernels(jp, cubins, err, &srcs)) {
-        prog->jit_of_step.assign(prog->steps.size(), -1);
-        set_error("qsv_program_jit: " + err);
-        return QSV_E_CUDA;
-    }
+    if (!compile_kernels(jp, cubins, err, &srcs))
+        return fail(QSV_E_CUDA, "qsv_program_jit: " + err);
     // load modules and functions
     const Driver& d = driver();
     cudaSetDevice(prog->ctx->device);
-    cudaFree(nullptr);  // make sure the primary context is current
-    prog->jit_kernels.assign(nk, {});
+    cudaFree(nullptr);  // make sure the primary context is current (also on a background thread)
+    b.kernels.assign(nk, {});
     for (int u = 0; u < nunits; ++u) {
         CUmodule mod;
         if (d.module_load(&mod, cubins[u].data()) != CUDA_SUCCESS) {
             // a stale or damaged cache entry: drop it and compile this unit afresh
             std::remove(unit_cache_path(srcs[u]).c_str());
-            if (!compile_unit(srcs[u], cubins[u], err, false) || d.module_load(&mod, cubins[u].data()) != CUDA_SUCCESS) {
-                prog->jit_of_step.assign(prog->steps.size(), -1);
-                set_error("qsv_program_jit: cuModuleLoadData failed" + (err.empty() ? std::string() : ": " + err));
-                return QSV_E_CUDA;
-            }
+            if (!compile_unit(srcs[u], cubins[u], err, false) || d.module_load(&mod, cubins[u].data()) != CUDA_SUCCESS)
+                return fail(QSV_E_CUDA, "qsv_program_jit: cuModuleLoadData failed" +
+                                            (err.empty() ? std::string() : ": " + err));
         }
-        prog->jit_modules.push_back(mod);
+        b.modules.push_back(mod);
         for (int k = u * per_unit; k < std::min(nk, (u + 1) * per_unit); ++k) {
             CUfunction f;
             const std::string name = "qsv_jit_" + std::to_string(k);
-            if (d.get_function(&f, mod, name.c_str()) != CUDA_SUCCESS) {
-                prog->jit_of_step.assign(prog->steps.size(), -1);
-                set_error("qsv_program_jit: cuModuleGetFunction failed for " + name);
-                return QSV_E_CUDA;
-            }
+            if (d.get_function(&f, mod, name.c_str()) != CUDA_SUCCESS)
+                return fail(QSV_E_CUDA, "qsv_program_jit: cuModuleGetFunction failed for " + name);
             const int K = kernel_k[k];
             const int mt = jp.kernel_mt[k];
             const size_t tile_smem = jit_tile_smem(K, mt);
             d.set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES,
                        static_cast<int>(std::min(tile_smem + kMaxBlobBytes, kSmemPerCta)));
-            prog->jit_kernels[k].func = f;
+            b.kernels[k].func = f;
             t_wide = jp.kernel_wide[k] != 0;
-            prog->jit_kernels[k].nt = threads_for_k(K) * mt;
+            b.kernels[k].nt = threads_for_k(K) * mt;
             t_wide = false;
-            prog->jit_kernels[k].mt = mt;
-            prog->jit_kernels[k].tile_smem = tile_smem;
+            b.kernels[k].mt = mt;
+            b.kernels[k].tile_smem = tile_smem;
         }
     }
-    for (auto& kv : prog->graphs)
+    b.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+// Installs a successful build (host thread; no run of the program is being enqueued).
+void jit_adopt(qsv_program* prog, JitBuild& b) {
+    prog->jit_of_step = std::move(b.jit_of_step);
+    prog->jit_kernels = std::move(b.kernels);
+    for (void* m : b.modules)
+        prog->jit_modules.push_back(m);
+    b.modules.clear();
+    for (auto& kv : prog->graphs)  // captured with the interpreter kernels
         cudaGraphExecDestroy(kv.second);
     prog->graphs.clear();
+}
+
+} // namespace
+
+int jit_program(qsv_program* prog, int max_kernels, double* seconds) {
+    if (int rc = jit_poll(prog, true); rc != QSV_OK)
+        return rc;
+    JitBuild b;
+    jit_build(prog, max_kernels, b);
+    if (b.rc != QSV_OK) {
+        prog->jit_of_step.assign(prog->steps.size(), -1);
+        set_error(b.err);
+        return b.rc;
+    }
+    jit_adopt(prog, b);
+    prog->jit_seconds = b.seconds;
     if (seconds)
-        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *seconds = b.seconds;
     return QSV_OK;
+}
+
+// Background compile: runs of the program use the interpreter kernel until the build is
+// adopted by jit_poll (at the start of the next run), so the first result does not wait for
+// NVRTC (UCCSD-28: ~170 s cold against a 16 s interpreted run).
+int jit_start_async(qsv_program* prog, int max_kernels) {
+    if (int rc = jit_poll(prog, true); rc != QSV_OK)
+        return rc;
+    for (const Step& s : prog->steps)
+        if (s.desc.kind == QSV_STEP_PASS && s.geom.K > 11) {  // no interpreter to run them meanwhile
+            double secs = 0;
+            return jit_program(prog, max_kernels, &secs);
+        }
+    prog->jit_build = new JitBuild;
+    prog->jit_done.store(false);
+    prog->jit_thread = std::thread([prog, max_kernels] {
+        jit_build(prog, max_kernels, *prog->jit_build);
+        prog->jit_done.store(true, std::memory_order_release);
+    });
+    return QSV_OK;
+}
+
+bool jit_pending(const qsv_program* prog) { return prog->jit_build != nullptr; }
+
+int jit_poll(qsv_program* prog, bool wait) {
+    if (!prog->jit_build)
+        return QSV_OK;
+    if (!wait && !prog->jit_done.load(std::memory_order_acquire))
+        return QSV_OK;
+    prog->jit_thread.join();
+    JitBuild* b = prog->jit_build;
+    prog->jit_build = nullptr;
+    int rc = b->rc;
+    if (rc == QSV_OK) {
+        cudaSetDevice(prog->ctx->device);
+        // every launch enqueued so far used the interpreter; the adoption only changes later ones
+        jit_adopt(prog, *b);
+        prog->jit_seconds = b->seconds;
+    } else {
+        set_error(b->err);
+    }
+    delete b;
+    return rc;
 }
 
 // Tensor map of a pass's tile on `st` (QSV_TMA_TENSOR=0 disables): the tile bits form
@@ -1230,6 +1309,14 @@ cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step
 }
 
 void jit_release(qsv_program* prog) {
+    if (prog->jit_build) {  // a background compile still running: wait, then drop its modules
+        prog->jit_thread.join();
+        const Driver& d = driver();
+        for (void* m : prog->jit_build->modules)
+            d.unload(static_cast<CUmodule>(m));
+        delete prog->jit_build;
+        prog->jit_build = nullptr;
+    }
     if (prog->jit_modules.empty())
         return;
     const Driver& d = driver();

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <complex>
 #include <cstring>
 #include <string>
@@ -1393,6 +1394,26 @@ extern "C" int qsv_program_jit(qsv_program* prog, int max_kernels, double* secon
     return qsv::jit_program(prog, max_kernels, seconds);
 }
 
+extern "C" int qsv_program_jit_async(qsv_program* prog, int max_kernels) {
+    QSV_REQUIRE(prog != nullptr, "qsv_program_jit_async: null program");
+    QSV_REQUIRE(max_kernels >= 0, "qsv_program_jit_async: max_kernels must be >= 0");
+    if (prog->ctx->nranks > 1) {  // every rank must switch kernels at the same run: compile now
+        double s = 0;
+        return qsv_program_jit(prog, max_kernels, &s);
+    }
+    return qsv::jit_start_async(prog, max_kernels);
+}
+
+extern "C" int qsv_program_jit_wait(qsv_program* prog, int block, int* done, double* seconds) {
+    QSV_REQUIRE(prog != nullptr, "qsv_program_jit_wait: null program");
+    const int rc = qsv::jit_poll(prog, block != 0);
+    if (done)
+        *done = qsv::jit_pending(prog) ? 0 : 1;
+    if (seconds)
+        *seconds = prog->jit_seconds;
+    return rc;
+}
+
 extern "C" int qsv_program_jit_info(qsv_program* prog, int* kernels, int* steps_jitted) {
     QSV_REQUIRE(prog != nullptr, "qsv_program_jit_info: null program");
     if (kernels)
@@ -1815,7 +1836,11 @@ extern "C" int qsv_program_run(qsv_state* st, qsv_program* prog) {
     if (int rc = qsv::check_aborted(ctx, "qsv_program_run"); rc != QSV_OK)
         return rc;
     QSV_CUDA(cudaSetDevice(ctx->device));
-    if (prog->has_collective || prog->steps.size() < 4 || ctx->trace_on)
+    if (qsv::jit_poll(prog, false) != QSV_OK) {  // a failed background compile: keep the interpreter
+        std::fprintf(stderr, "qsv: background JIT failed, using the interpreter pass kernel (%s)\n",
+                     qsv_last_error());
+    }
+    if (prog->has_collective || prog->steps.size() < 4 || ctx->trace_on || qsv::jit_pending(prog))
         return enqueue_steps(st, prog, nullptr);
     auto it = prog->graphs.find(st->amps);
     if (it == prog->graphs.end()) {
@@ -1846,6 +1871,8 @@ extern "C" int qsv_program_profile(qsv_state* st, qsv_program* prog, float* ms_o
     QSV_REQUIRE(st != nullptr && prog != nullptr && ms_out != nullptr, "qsv_program_profile: null argument");
     qsv_ctx* ctx = st->ctx;
     QSV_CUDA(cudaSetDevice(ctx->device));
+    if (qsv::jit_poll(prog, false) != QSV_OK)
+        std::fprintf(stderr, "qsv: background JIT failed, using the interpreter pass kernel (%s)\n", qsv_last_error());
     const size_t n = prog->steps.size();
     std::vector<cudaEvent_t> evs(n + 1);
     for (auto& e : evs)

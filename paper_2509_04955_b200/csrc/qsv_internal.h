@@ -11,6 +11,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "device_types.h"
@@ -116,6 +117,7 @@ struct JitKernel {
     int mt = 1;
     size_t tile_smem = 0;
 };
+struct JitBuild;             // compiled + loaded kernels not yet adopted by the program (jit.cu)
 } // namespace qsv
 
 struct qsv_program {
@@ -128,6 +130,12 @@ struct qsv_program {
     std::vector<int> jit_of_step;              // JIT kernel per step, -1 = interpreter
     std::vector<qsv::JitKernel> jit_kernels;
     std::vector<void*> jit_modules;            // CUmodule
+    // background compile (qsv_program_jit_async): the thread fills `jit_build` and sets
+    // jit_done; the host thread adopts the kernels at the next run (interpreter until then)
+    std::thread jit_thread;
+    std::atomic<bool> jit_done{false};
+    qsv::JitBuild* jit_build = nullptr;
+    double jit_seconds = 0;                    // compile + load time of the adopted kernels
     bool has_collective = false;
     // one captured graph per state buffer it was run on
     std::map<const void*, cudaGraphExec_t> graphs;
@@ -164,6 +172,10 @@ cudaError_t launch_pass(const qsv_state* st, const Step& step, const unsigned ch
 // NVRTC specialisation (jit.cu).
 bool jit_available(std::string& why);
 int jit_program(qsv_program* prog, int max_kernels, double* seconds);
+int jit_start_async(qsv_program* prog, int max_kernels);
+// adopts a finished background compile (waits for it when `wait`); returns QSV_OK while it runs
+int jit_poll(qsv_program* prog, bool wait);
+bool jit_pending(const qsv_program* prog);
 // Host-only: NVRTC-compiles the distinct pass kernels of compiled steps (no device).
 int jit_check(const std::vector<Step>& steps, const unsigned char* host_blobs, int max_kernels, int* kernels);
 cudaError_t launch_jit(const qsv_program* prog, const qsv_state* st, size_t step, const unsigned char* d_blob,

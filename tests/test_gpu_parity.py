@@ -316,3 +316,40 @@ def test_race_checks_poison_and_grid():
     for env in ({"QSV_DEBUG_POISON": "1"}, {"QSV_DEBUG_GRID": "1"}, {"QSV_DEBUG_GRID": "7", "QSV_DEBUG_POISON": "1"},
                 {"QSV_DEBUG_POISON": "1", "QSV_TMA_TENSOR": "0"}):  # tensor-map and per-run bulk copies
         assert _sanitize_digests(env) == base, env
+
+
+@pytest.mark.timeout(900)
+def test_background_jit_switches_kernels(tmp_path, monkeypatch):
+    """PlanOptions(jit=2): NVRTC compiles on a host thread while runs use the interpreter
+    kernel; after jit_wait the runs use the specialised kernels.  Both results match the
+    oracle, and the post-switch run is bitwise the synchronously compiled engine's."""
+    monkeypatch.setenv("QSV_JIT_CACHE", str(tmp_path))  # cold: the compile takes seconds
+    c = pkg.Circuit.generate("uccsd:20:3000:3")
+    ref = O.run_local(c)
+    e = pkg.Engine(c, pkg.PlanOptions(jit=2))
+    try:
+        e.set_basis(0)
+        e.run()
+        e.sync()
+        interpreted_first = e.jit_info()["kernels"] == 0
+        first = e.download()
+        e.jit_wait()
+        info = e.jit_info()
+        assert info["kernels"] > 0 and info["seconds"] > 0
+        e.set_basis(0)
+        e.run()
+        e.sync()
+        second = e.download()
+    finally:
+        e.close()
+    assert interpreted_first  # hundreds of kernels compile far slower than one interpreted run
+    assert np.abs(first - ref).max() <= 1e-10
+    assert np.abs(second - ref).max() <= 1e-10
+    s = pkg.Engine(c, pkg.PlanOptions())
+    try:
+        s.set_basis(0)
+        s.run()
+        s.sync()
+        assert np.array_equal(s.download(), second)
+    finally:
+        s.close()
