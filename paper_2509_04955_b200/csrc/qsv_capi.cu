@@ -1570,7 +1570,8 @@ int enqueue_steps(qsv_state* st, qsv_program* prog, cudaEvent_t* evs) {
     size_t first = 0;
     bool basis_start = false;
     if (evs == nullptr && ctx->nranks > 1 && ctx->comm != nullptr && !prog->steps.empty() &&
-        prog->steps[0].desc.kind == QSV_STEP_SWAP && env_int("QSV_BASIS_SWAPS", 1) != 0) {
+        prog->steps[0].desc.kind == QSV_STEP_SWAP && env_int("QSV_BASIS_SWAPS", 1) != 0 &&
+        env_int("QSV_OVERLAP", 0) == 0) {  // the region-overlap schedule pairs passes with every swap
         QSV_CUDA(cudaSetDevice(ctx->device));
         if (int rc = agree_basis(st, &basis_start); rc != QSV_OK)
             return rc;

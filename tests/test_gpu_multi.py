@@ -124,7 +124,7 @@ def test_cross_p_bitwise(two, spec):
 
 @pytest.mark.parametrize("mode", [{"QSV_SWAP_MODE": "nccl"}, {"QSV_OVERLAP": "1"},
                                   {"QSV_OVERLAP": "1", "QSV_SWAP_MODE": "nccl"}])
-@pytest.mark.parametrize("spec", ["random:20:10:2", "qaoa:18:2:1", "uccsd:18:600:3"])
+@pytest.mark.parametrize("spec", ["random:20:10:2", "qaoa:18:2:1", "uccsd:18:600:3", "qft:18"])
 def test_two_gpu_swap_paths(two, spec, mode, monkeypatch):
     """The NCCL chunked swap and the (opt-in) region-overlap schedules give the same
     amplitudes as the oracle (the default P2P swap is covered above)."""
