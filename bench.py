@@ -350,9 +350,19 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
            "stream events (H2D(k+1) | run(k) | D2H(k-1)); pinned host buffers, full state in and out"
            if ne > 1 else
            "qsim_engine_upload -> qsim_engine_run -> qsim_engine_download (pinned host buffers, full state in and out)")
-    return {"value": gates / e2e_s, "unit": "gates/s", "steps": nsteps, "h2d_bytes_per_step": 16 * N * world,
-            "d2h_bytes_per_step": 16 * N * world, "seconds_per_step": e2e_s, "engines": ne,
-            "host_norm_rank_shard": local_norm, "api": api}
+    out = {"value": gates / e2e_s, "unit": "gates/s", "steps": nsteps, "h2d_bytes_per_step": 16 * N * world,
+           "d2h_bytes_per_step": 16 * N * world, "seconds_per_step": e2e_s, "engines": ne,
+           "host_norm_rank_shard": local_norm, "api": api}
+    # the bound: this GPU's PCIe with both directions busy (tools/pcie_probe.py on this pool)
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_pcie_probe.json")) as f:
+            duplex = float(json.load(f)["duplex_total_gbs"])
+        floor_s = 2 * 16 * N / (duplex * 1e9)  # per GPU: its shard in and out over its own link
+        out["pcie_roofline"] = {"duplex_gbs_measured": duplex, "floor_s_per_step": floor_s,
+                                "frac": floor_s / e2e_s, "source": "profiles/r02_pcie_probe.json"}
+    except (OSError, KeyError, ValueError):
+        pass
+    return out
 
 
 # Native libraries (NCCL's version banner, CUDA warnings) may write to fd 1; the
