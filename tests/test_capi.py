@@ -108,3 +108,15 @@ def test_gather_cap_refused_without_gpu(monkeypatch):
     rc = pkg.load_qsim().qsim_run_distributed(c._h, 1, 8, 2, None, C.byref(o),
                                               out.view(np.float64).ctypes.data_as(C.POINTER(C.c_double)), None)
     assert rc != 0 and b"cap" in pkg.load_qsim().qsim_last_error()
+
+
+def test_background_jit_entry_points_validate_arguments():
+    """qsv_program_jit_async / _wait and qsim_engine_jit_wait reject null handles (no device
+    needed), and PlanOptions(jit=2) reaches the C struct unchanged."""
+    Q, L = pkg.load_qsv(), pkg.load_qsim()
+    assert Q.qsv_program_jit_async(None, 8) != 0
+    done = C.c_int(-1)
+    assert Q.qsv_program_jit_wait(None, 1, C.byref(done), None) != 0
+    assert L.qsim_engine_jit_wait(None) != 0
+    assert pkg.PlanOptions(jit=2).to_c().jit == 2
+    assert pkg.PlanOptions().to_c().jit == 1
