@@ -353,8 +353,12 @@ def e2e_stream(args, pkg, qsv, eng, circ, opts, n_local, gates, rank, world, loc
     out = {"value": gates / e2e_s, "unit": "gates/s", "steps": nsteps, "h2d_bytes_per_step": 16 * N * world,
            "d2h_bytes_per_step": 16 * N * world, "seconds_per_step": e2e_s, "engines": ne,
            "host_norm_rank_shard": local_norm, "api": api}
-    # the bound: this GPU's PCIe with both directions busy (tools/pcie_probe.py on this pool)
+    # the bound at N = 1: this GPU's PCIe with both directions busy (tools/pcie_probe.py on this
+    # pool); with N > 1 the GPUs share the host's memory and root complexes, which the probe of
+    # one link does not bound, so no roofline is claimed there
     try:
+        if world != 1:
+            raise ValueError("multi-GPU")
         with open(os.path.join(ROOT, "profiles", "r02_pcie_probe.json")) as f:
             duplex = float(json.load(f)["duplex_total_gbs"])
         floor_s = 2 * 16 * N / (duplex * 1e9)  # per GPU: its shard in and out over its own link
