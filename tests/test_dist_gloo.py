@@ -208,3 +208,25 @@ def test_multi_swap_index_math(k):
         seq = _pair_swap_emulated(seq, l, g, v)
     for a, b in zip(merged, seq):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("x", [0, 0b1010011, 0b1111111, 0b0100100])
+def test_basis_start_swap_relabel_index_math(x):
+    """csrc/qsv_capi.cu enqueue_steps: leading qubit swaps on a basis state |x> become x with
+    bits g and v exchanged (the single 1 moves; no transfer).  Checked on the host against the
+    pairwise swap's data movement (the kernel's index math) for a run of swaps on 4 ranks."""
+    l, R = 5, 4
+    shards = [np.zeros(1 << l, dtype=np.complex128) for _ in range(R)]
+    shards[x >> l][x & ((1 << l) - 1)] = 1.0
+    seq = [(5, 2), (6, 0), (5, 4)]  # (global g, local v) in program order
+    moved = shards
+    for g, v in seq:
+        moved = _pair_swap_emulated(moved, l, g, v)
+    y = x
+    for g, v in seq:
+        if ((y >> g) & 1) != ((y >> v) & 1):
+            y ^= (1 << g) | (1 << v)
+    want = [np.zeros(1 << l, dtype=np.complex128) for _ in range(R)]
+    want[y >> l][y & ((1 << l) - 1)] = 1.0
+    for a, b in zip(moved, want):
+        assert np.array_equal(a, b)
